@@ -1,0 +1,499 @@
+"""Benchmark of the PCCL collective data plane on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload auto|hash|allreduce|quant|local]
+                    [--impl ours|reference]
+
+Workloads (BASELINE.json metric "All-reduce bus GB/s (1 GiB fp32, 2/4/8 B200);
+quant/hash kernel HBM GB/s"):
+
+* ``hash`` (default at N=1; config 4): simplehash of an 8.03 B-parameter bf16
+  shared state laid out like Llama-3-8B (291 entries, 16.06 GB per GPU), one
+  multi-entry launch per step; value = HBM GB/s (bytes hashed / time). At N>1
+  every GPU hashes its own replica (replicas only: sync_shared_state hashes
+  each peer's copy) and value is the aggregate.
+* ``allreduce`` (default at N>1; config 2): in-place AVG all-reduce of 1 GiB
+  fp32 per GPU over NVLink, W = N ring positions; value = bus GB/s
+  (algbw * 2(W-1)/W, algbw = 1 GiB / max-over-ranks time).
+* ``quant`` (config 3): u8-quantized AVG all-reduce of 1.2 B fp32 per GPU.
+* ``local``: W=8 logical peers of 1 GiB each on one GPU (the reference's
+  in-process RingSession shape); value = bus GB/s.
+
+Inputs are synthetic (torch RNG) and larger than L2 (126 MB), so no L2 flush
+is needed between steps. Timing: CUDA events on the launching stream, W >= 3
+warm-up steps, barrier + synchronize around the timed region, max over ranks.
+``--impl reference`` times the reference algorithm's CPU restatement (the
+oracle port; the reference itself is pure Python/NumPy) on host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "All-reduce bus GB/s (1 GiB fp32, 2/4/8 B200); quant/hash kernel HBM GB/s"
+
+
+def llama3_8b_layout() -> list[tuple[str, int]]:
+    """(name, elements) of a Llama-3-8B-like state: 291 entries, 8.03 B params."""
+    d, kv, ff, vocab, layers = 4096, 1024, 14336, 128256, 32
+    out = [("embed", vocab * d)]
+    for i in range(layers):
+        out += [
+            (f"l{i}.q", d * d), (f"l{i}.k", kv * d), (f"l{i}.v", kv * d), (f"l{i}.o", d * d),
+            (f"l{i}.gate", ff * d), (f"l{i}.up", ff * d), (f"l{i}.down", d * ff),
+            (f"l{i}.attn_norm", d), (f"l{i}.mlp_norm", d),
+        ]
+    out += [("norm", d), ("lm_head", vocab * d)]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            self.out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "src": "measured"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_init(n: int):
+    import torch
+    import torch.distributed as dist
+
+    if n <= 1 and "RANK" not in os.environ:
+        return 0, 1, 0
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(n)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def bench_hash(args, rank, world, local):
+    import torch
+
+    from paper_2505_14065_b200 import _native
+    from paper_2505_14065_b200.sharedstate import simplehash_many_async
+
+    dev = torch.device("cuda", local)
+    layout = llama3_8b_layout()
+    total_elems = sum(n for _, n in layout)
+    state = torch.empty(total_elems, dtype=torch.bfloat16, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # random bf16 bit patterns (fills all 16 GB quickly)
+    state.view(torch.int16).random_(-32768, 32767, generator=g)
+    views, off = [], 0
+    for _, n in layout:
+        views.append(state[off : off + n])
+        off += n
+    nbytes = total_elems * 2
+    out = torch.empty(len(views), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        simplehash_many_async(views, out)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        simplehash_many_async(views, out)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / args.steps
+    clk = clocks.stop()
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
+    launches = args.steps  # one multi-entry launch per step
+
+    # single largest entry alone: chain-latency bound reference point
+    big = views[0]
+    t0.record(stream)
+    for _ in range(3):
+        simplehash_many_async([big], out[:1])
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    big_ms = t0.elapsed_time(t1) / 3
+
+    # e2e: host state (pinned) -> device, hash, digests -> host
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(total_elems, dtype=torch.bfloat16, pin_memory=True)
+        host.copy_(state, non_blocking=False)
+        digests = torch.empty(len(views), dtype=torch.int64, pin_memory=True)
+        def e2e_step():
+            state.copy_(host, non_blocking=True)
+            simplehash_many_async(views, out)
+            digests.copy_(out, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        k = max(1, min(args.steps, 3))
+        barrier(world)
+        t0.record(stream)
+        for _ in range(k):
+            e2e_step()
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(t0.elapsed_time(t1) / k, world)
+        e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": len(views) * 8, "ms_per_step": round(e2e_ms, 3)}
+        del host
+
+    pk = peaks()
+    achieved = nbytes / (ms * 1e-3) / 1e9
+    result = {
+        "value": round(world * nbytes / (ms_max * 1e-3) / 1e9, 2),
+        "unit": "GB/s",
+        "ms_per_step": round(ms_max, 4),
+        "scaling": "weak",
+        "dtype": "u8",
+        "config": {"workload": "config4-hash: simplehash of Llama-3-8B-like bf16 shared state (291 entries, 16.06 GB/GPU), one multi-entry launch per step",
+                   "entries": len(views), "bytes_per_gpu": nbytes, "largest_entry_bytes": views[0].numel() * 2,
+                   "l2": "inputs 16 GB >> 126 MB L2; no flush needed", "replicas": world},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
+                     "kernel": "simplehash_batch_kernel", "algorithmic_bytes_per_launch": nbytes,
+                     "largest_entry_alone_ms": round(big_ms, 3),
+                     "largest_entry_alone_gbs": round(views[0].numel() * 2 / (big_ms * 1e-3) / 1e9, 1)},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_hash_baseline(layout)
+    return result
+
+
+def hash_sample(layout):
+    """Bounded CPU sample of the config-4 workload: every 9th entry (largest
+    first order keeps one 1.05 GB embedding), random bytes."""
+    import numpy as np
+
+    sel = [n for i, (_, n) in enumerate(layout) if i % 9 == 0]
+    rng = np.random.default_rng(7)
+    return [rng.integers(0, 256, 2 * n, dtype=np.uint8) for n in sel]
+
+
+def cpu_hash_baseline(layout) -> dict:
+    from oracle import simplehash as osh
+
+    bufs = hash_sample(layout)
+    threads = os.cpu_count() or 1
+    nb = sum(b.size for b in bufs)
+    t = time.perf_counter()
+    osh.simplehash_many_c(bufs, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{len(bufs)} of 291 config-4 entries ({nb / 1e9:.2f} GB), oracle/simplehash.c on {threads} threads"}
+
+
+def bench_allreduce(args, rank, world, local, quantize=False):
+    import torch
+
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
+
+    dev = torch.device("cuda", local)
+    n = args.elems or ((1 << 28) if not quantize else 1_200_000_000)
+    op = "avg"
+    g = torch.Generator(device=dev).manual_seed(rank)
+    src = torch.randn(n, generator=g, device=dev) * (1e-2 if quantize else 1.0)
+    buf = torch.empty_like(src)
+    esz = 4
+    ring = DeviceRing(device=dev, capacity_bytes=16384 + n * esz + 4 * (n // world + 1) * esz + (1 << 20))
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        buf.copy_(src)
+        ring.run_all_reduce(buf, op, quantize=quantize)
+    torch.cuda.synchronize(dev)
+    # time K ops back to back; each op blocks on its own completion (engine semantics)
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    total = 0.0
+    for _ in range(args.steps):
+        buf.copy_(src)  # fresh input each step (outside the op's events)
+        e0.record(stream)
+        ring.run_all_reduce(buf, op, quantize=quantize)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        total += e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ms = total / args.steps
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
+    S = n * esz
+    algbw = S / (ms_max * 1e-3) / 1e9
+    busbw = algbw * 2 * (world - 1) / world if world > 1 else 0.0
+    # e2e: pinned host buffer -> device, all-reduce, result -> host
+    e2e = None
+    if not args.no_e2e:
+        host_in = src.cpu().pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        k = max(1, min(args.steps, 3))
+        barrier(world)
+        tt = 0.0
+        for _ in range(k):
+            e0.record(stream)
+            buf.copy_(host_in, non_blocking=True)
+            ring.run_all_reduce(buf, op, quantize=quantize)
+            host_out.copy_(buf, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            tt += e0.elapsed_time(e1)
+        e2e_ms = max_over_ranks(tt / k, world)
+        e2e_alg = S / (e2e_ms * 1e-3) / 1e9
+        e2e = {"value": round(e2e_alg * 2 * (world - 1) / world if world > 1 else e2e_alg, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3)}
+    nvl_bytes = 2 * (world - 1) / world * S  # per-GPU NVLink ingress
+    launches_per_op = (2 + 2 + 1) if not quantize else (1 + 3 * (world - 1) + 2 + 1)
+    result = {
+        "value": round(busbw, 2),
+        "unit": "GB/s",
+        "ms_per_step": round(ms_max, 4),
+        "scaling": "weak",
+        "dtype": "f32",
+        "config": {"workload": f"config{'3' if quantize else '2'}: in-place AVG all-reduce{' u8-quantized' if quantize else ''} of {S / 2**30:.3f} GiB fp32 per GPU over NVLink, W={world}",
+                   "elements_per_gpu": n, "ring": list(range(world)), "algbw_GBps": round(algbw, 2),
+                   "busbw_definition": "algbw*2(W-1)/W", "l2": "1 GiB inputs > 126 MB L2"},
+        "roofline": {"bound": "nvlink", "achieved": round(nvl_bytes / (ms_max * 1e-3) / 1e9, 1),
+                     "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                     "frac": round(nvl_bytes / (ms_max * 1e-3) / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
+                     "peak_src": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": launches_per_op * args.steps,
+    }
+    ring.close()
+    return result
+
+
+def bench_local(args, rank, world, local):
+    import torch
+
+    from paper_2505_14065_b200 import LocalRing
+
+    dev = torch.device("cuda", local)
+    w = 8
+    n = args.elems or (1 << 28)
+    g = torch.Generator(device=dev).manual_seed(0)
+    srcs = [torch.randn(n, generator=g, device=dev) for _ in range(w)]
+    bufs = [torch.empty_like(s) for s in srcs]
+    ring = LocalRing(w, device=dev, backup=False)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        ring.launch(bufs, "avg")
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ring.launch(bufs, "avg")
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    S = n * 4
+    busbw = S / (ms * 1e-3) / 1e9 * 2 * (w - 1) / w
+    hbm = 2 * w * S / (ms * 1e-3) / 1e9  # W reads + W writes per element
+    pk = peaks()
+    return {
+        "value": round(busbw, 2), "unit": "GB/s", "ms_per_step": round(ms, 4), "scaling": "weak", "dtype": "f32",
+        "config": {"workload": "8 logical ring peers x 1 GiB fp32 on one GPU, AVG (RingSession shape)", "elements_per_peer": n},
+        "roofline": {"bound": "hbm", "achieved": round(hbm, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(hbm / pk["hbm_gbs"], 4), "traffic": None, "kernel": "local_fold_all_kernel"},
+        "clocks": clk, "e2e": None, "gpu_launches": args.steps,
+    }
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm on host cores (oracle port)
+# ---------------------------------------------------------------------------
+def reference_arm(args, workload, world):
+    import numpy as np
+
+    if workload == "hash":
+        layout = llama3_8b_layout()
+        bufs = hash_sample(layout)
+        from oracle import simplehash as osh
+
+        threads = os.cpu_count() or 1
+        nb = sum(b.size for b in bufs)
+        for _ in range(min(args.warmup, 1)):
+            osh.simplehash_many_c(bufs[-4:], threads=threads)
+        t = time.perf_counter()
+        steps = max(1, min(args.steps, 2))
+        for _ in range(steps):
+            osh.simplehash_many_c(bufs, threads=threads)
+        dt = (time.perf_counter() - t) / steps
+        v = round(world * nb / dt / 1e9, 3)
+        return {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": world,
+                "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": "config4-hash (bounded sample)"},
+                "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
+                                 "sample": f"{len(bufs)} of 291 entries ({nb / 1e9:.2f} GB) via oracle/simplehash.c"},
+                "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    from oracle import ring as oring
+
+    w = max(world, 2)
+    n = 1 << 22  # bounded sample: 16 MiB per rank
+    rng = np.random.default_rng(0)
+    bufs = [rng.normal(0, 1, n).astype(np.float32) for _ in range(w)]
+    quant = workload == "quant"
+    oring.ring_allreduce(bufs, oring.ReduceOp.AVG, quantize=quant)
+    steps = max(1, min(args.steps, 3))
+    t = time.perf_counter()
+    for _ in range(steps):
+        oring.ring_allreduce(bufs, oring.ReduceOp.AVG, quantize=quant)
+    dt = (time.perf_counter() - t) / steps
+    algbw = n * 4 / dt / 1e9
+    v = round(algbw * 2 * (w - 1) / w, 4)
+    return {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{workload} W={w} (bounded sample 16 MiB/rank)"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "port",
+                             "sample": f"oracle.ring.ring_allreduce W={w}, 4 Mi f32 per rank, AVG{' u8' if quant else ''}"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "local"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--elems", type=int, default=0, help="override elements per GPU (allreduce/quant/local)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world_env = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    workload = args.workload
+    if workload == "auto":
+        workload = "hash" if world_env <= 1 else "allreduce"
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        print(json.dumps(reference_arm(args, workload, world_env)))
+        return
+
+    rank, world, local = dist_init(args.gpus)
+    if workload == "hash":
+        res = bench_hash(args, rank, world, local)
+    elif workload == "allreduce":
+        res = bench_allreduce(args, rank, world, local, quantize=False)
+    elif workload == "quant":
+        res = bench_allreduce(args, rank, world, local, quantize=True)
+    else:
+        res = bench_local(args, rank, world, local)
+    line = {"metric": METRIC, "value": res.pop("value"), "unit": res.pop("unit"), "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res.pop("ms_per_step"),
+            "higher_is_better": True, "scaling": res.pop("scaling"), "vs_baseline": None,
+            "dtype": res.pop("dtype"), "data": "synthetic"}
+    line.update(res)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,105 @@
+// Per-element functors of the quantization kernels, shared by the single-GPU
+// seams (kernels.cu) and the NVLink ring (ring_ipc.cu). See ew_loop().
+#pragma once
+
+#include "elementwise.cuh"
+#include "numerics.cuh"
+
+namespace pcclb {
+
+// ---------------------------------------------------------------------------
+// K2 range
+// ---------------------------------------------------------------------------
+struct RangeF {
+  const float *__restrict__ x;
+  RangeAcc acc;
+  __device__ __forceinline__ void one(uint64_t i) { acc.add(x[i]); }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<float> a = ld16_cs(x + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc.add(a.e[k]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K3/K6 quantize (+ optional adoption D(Q(x)) / avg_div)
+// ---------------------------------------------------------------------------
+struct QuantF {
+  const float *__restrict__ x;
+  uint8_t *__restrict__ codes;
+  float *__restrict__ adopt;  // may alias x (adoption in place): same element, same thread
+  QParams qp;
+  float avg;  // 1 => no division
+  bool do_div;
+  __device__ __forceinline__ float adopt_val(uint32_t q) {
+    float d = dequant1(q, qp.mn, qp.scale);
+    return do_div ? x86_div(d, avg) : d;
+  }
+  __device__ __forceinline__ void one(uint64_t i) {
+    uint32_t q = quant1(x[i], qp.mn, qp.scale);
+    codes[i] = (uint8_t)q;
+    if (adopt) adopt[i] = adopt_val(q);
+  }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<float> a = ld16(x + i);
+    uint32_t q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = quant1(a.e[k], qp.mn, qp.scale);
+    *reinterpret_cast<uint32_t *>(codes + i) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    if (adopt) {
+      Pack16<float> d;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d.e[k] = adopt_val(q[k]);
+      st16(adopt + i, d);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K4/K7 dequantize (+ optional AVG division)
+// ---------------------------------------------------------------------------
+struct DequantF {
+  float *__restrict__ out;
+  const uint8_t *__restrict__ codes;
+  float mn, scale, avg;
+  bool do_div;
+  __device__ __forceinline__ float val(uint32_t q) {
+    float d = dequant1(q, mn, scale);
+    return do_div ? x86_div(d, avg) : d;
+  }
+  __device__ __forceinline__ void one(uint64_t i) { out[i] = val(codes[i]); }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    uint32_t q = *reinterpret_cast<const uint32_t *>(codes + i);
+    Pack16<float> d;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d.e[k] = val((q >> (8 * k)) & 0xffu);
+    st16(out + i, d);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K5 dequant-accumulate (+ fused range of the result)
+// ---------------------------------------------------------------------------
+template <int OP>
+struct DequantAccF {
+  float *__restrict__ acc;
+  const uint8_t *__restrict__ codes;
+  float mn, scale;
+  bool track;
+  RangeAcc r;
+  __device__ __forceinline__ float step(float local, uint32_t q) {
+    float v = reduce_op<OP>(local, dequant1(q, mn, scale));
+    if (track) r.add(v);
+    return v;
+  }
+  __device__ __forceinline__ void one(uint64_t i) { acc[i] = step(acc[i], codes[i]); }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<float> a = ld16(acc + i);
+    uint32_t q = *reinterpret_cast<const uint32_t *>(codes + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a.e[k] = step(a.e[k], (q >> (8 * k)) & 0xffu);
+    st16(acc + i, a);
+  }
+};
+
+}  // namespace pcclb

@@ -1,0 +1,254 @@
+// Single-GPU kernel seams of the ring data plane.
+//
+//   pcclb_accumulate            K1  collective.py:66-71, :407, :416
+//   pcclb_finalize              K8  collective.py:479-482
+//   pcclb_range_f32             K2  collective.py:117-121
+//   pcclb_quantize_u8           K3/K6 collective.py:119-129, :538-551
+//   pcclb_dequantize_u8         K4/K7 collective.py:132-135, :445-452
+//   pcclb_dequant_accumulate_u8 K5  collective.py:399-409
+//
+// All are HBM-bound streaming kernels: 128-bit vector loads/stores, grid
+// sized to a multiple of the SM count, arithmetic from numerics.cuh.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "numerics.cuh"
+#include "ew_ops.cuh"
+
+namespace pcclb {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+// ---------------------------------------------------------------------------
+// K1 accumulate
+// ---------------------------------------------------------------------------
+template <typename T, int OP>
+struct AccumulateF {
+  T *__restrict__ acc;
+  const T *__restrict__ in;
+  __device__ __forceinline__ void one(uint64_t i) { acc[i] = reduce_op<OP>(acc[i], in[i]); }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<T> a = ld16(acc + i), b = ld16_cs(in + i);
+#pragma unroll
+    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = reduce_op<OP>(a.e[k], b.e[k]);
+    st16(acc + i, a);
+  }
+};
+
+template <typename T, int OP, int VEC>
+__global__ void __launch_bounds__(kThreads) accumulate_kernel(T *acc, const T *in, uint64_t n,
+                                                               uint64_t head) {
+  AccumulateF<T, OP> f{acc, in};
+  ew_loop<VEC, kUnroll>(n, head, f);
+}
+
+template <typename T, int OP>
+static int launch_accumulate(T *acc, const T *in, uint64_t n, cudaStream_t s) {
+  if (n == 0) return PCCLB_OK;
+  uint64_t head = peel16<T>(acc);
+  bool vec_ok = peel16<T>(in) == head;
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * (16 / sizeof(T)));
+  if (vec_ok)
+    accumulate_kernel<T, OP, 16 / sizeof(T)><<<grid, kThreads, 0, s>>>(acc, in, n, head);
+  else
+    accumulate_kernel<T, OP, 1><<<grid, kThreads, 0, s>>>(acc, in, n, 0);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+template <typename T>
+static int dispatch_accumulate(void *acc, const void *in, uint64_t n, int op, cudaStream_t s) {
+  T *a = static_cast<T *>(acc);
+  const T *b = static_cast<const T *>(in);
+  switch (op) {
+    case PCCLB_SUM:
+    case PCCLB_AVG:
+      return launch_accumulate<T, PCCLB_SUM>(a, b, n, s);
+    case PCCLB_MAX:
+      return launch_accumulate<T, PCCLB_MAX>(a, b, n, s);
+    case PCCLB_MIN:
+      return launch_accumulate<T, PCCLB_MIN>(a, b, n, s);
+  }
+  return PCCLB_EINVAL;
+}
+
+// ---------------------------------------------------------------------------
+// K8 finalize: buf /= dtype(W)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DivF {
+  T *__restrict__ buf;
+  T w;
+  __device__ __forceinline__ void one(uint64_t i) { buf[i] = x86_div(buf[i], w); }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<T> a = ld16(buf + i);
+#pragma unroll
+    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = x86_div(a.e[k], w);
+    st16(buf + i, a);
+  }
+};
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) div_kernel(T *buf, uint64_t n, uint64_t head, T w) {
+  DivF<T> f{buf, w};
+  ew_loop<VEC, kUnroll>(n, head, f);
+}
+
+template <typename T>
+static int launch_div(T *buf, uint64_t n, uint32_t w, cudaStream_t s) {
+  if (n == 0) return PCCLB_OK;
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * (16 / sizeof(T)));
+  div_kernel<T, 16 / sizeof(T)><<<grid, kThreads, 0, s>>>(buf, n, peel16<T>(buf), (T)w);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+// K2 range
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) range_kernel(const float *x, uint64_t n, uint64_t head,
+                                                          pcclb_range *out) {
+  RangeF f{x, RangeAcc()};
+  ew_loop<VEC, kUnroll>(n, head, f);
+  range_block_commit(f.acc, out);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads)
+    quantize_kernel(const float *x, uint64_t n, uint64_t head, const pcclb_range *range,
+                    uint8_t *codes, pcclb_qmeta *meta, float *adopt, uint32_t avg_div) {
+  QParams qp = qparams_from_range(*range);
+  if (meta && blockIdx.x == 0 && threadIdx.x == 0) {
+    meta->min_val = qp.mn;
+    meta->scale = qp.scale;
+  }
+  QuantF f{x, codes, adopt, qp, (float)avg_div, avg_div > 1};
+  ew_loop<VEC, kUnroll>(n, head, f);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads)
+    dequantize_kernel(float *out, const uint8_t *codes, uint64_t n, uint64_t head,
+                      const pcclb_qmeta *meta, uint32_t avg_div) {
+  DequantF f{out, codes, meta->min_val, meta->scale, (float)avg_div, avg_div > 1};
+  ew_loop<VEC, kUnroll>(n, head, f);
+}
+
+template <int OP, int VEC>
+__global__ void __launch_bounds__(kThreads)
+    dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, uint64_t head,
+                       const pcclb_qmeta *meta, pcclb_range *next) {
+  DequantAccF<OP> f{acc, codes, meta->min_val, meta->scale, next != nullptr, RangeAcc()};
+  ew_loop<VEC, kUnroll>(n, head, f);
+  if (next) range_block_commit(f.r, next);
+}
+
+// float/code pointer pair vectorizable with the same peel?
+static bool fc_vec_ok(const float *x, const uint8_t *codes, uint64_t *head) {
+  uint64_t h = peel16<float>(x);
+  *head = h;
+  return ((reinterpret_cast<uintptr_t>(codes) + h) & 3) == 0;
+}
+
+}  // namespace pcclb
+
+using namespace pcclb;
+
+extern "C" {
+
+int pcclb_accumulate(void *acc, const void *in, uint64_t n, int dtype, int op, void *stream) {
+  if (!valid_dtype(dtype) || !valid_op(op) || (n && (!acc || !in))) return PCCLB_EINVAL;
+  if (dtype == PCCLB_F32) return dispatch_accumulate<float>(acc, in, n, op, as_stream(stream));
+  return dispatch_accumulate<double>(acc, in, n, op, as_stream(stream));
+}
+
+int pcclb_finalize(void *buf, uint64_t n, int dtype, int op, uint32_t world, void *stream) {
+  if (!valid_dtype(dtype) || !valid_op(op) || world < 1 || (n && !buf)) return PCCLB_EINVAL;
+  if (op != PCCLB_AVG) return PCCLB_OK;
+  if (dtype == PCCLB_F32) return launch_div<float>((float *)buf, n, world, as_stream(stream));
+  return launch_div<double>((double *)buf, n, world, as_stream(stream));
+}
+
+int pcclb_range_reset(pcclb_range *d_range, uint32_t count, void *stream) {
+  if (!d_range) return PCCLB_EINVAL;
+  PCCLB_CUDA(cudaMemsetAsync(d_range, 0, sizeof(pcclb_range) * count, as_stream(stream)));
+  return PCCLB_OK;
+}
+
+int pcclb_range_f32(const float *x, uint64_t n, pcclb_range *d_range, void *stream) {
+  if (!d_range || (n && !x)) return PCCLB_EINVAL;
+  if (n == 0) return PCCLB_OK;
+  cudaStream_t s = as_stream(stream);
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * 4);
+  range_kernel<4><<<grid, kThreads, 0, s>>>(x, n, peel16<float>(x), d_range);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+int pcclb_quantize_u8(const float *x, uint64_t n, const pcclb_range *d_range, uint8_t *codes,
+                      pcclb_qmeta *d_meta, float *adopt_out, uint32_t avg_div, void *stream) {
+  if (!d_range || (n && (!x || !codes)) || avg_div < 1) return PCCLB_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  uint64_t head;
+  bool ok = fc_vec_ok(x, codes, &head);
+  if (adopt_out && peel16<float>(adopt_out) != head) ok = false;
+  unsigned grid = grid_for(n ? n : 1, (uint64_t)kThreads * kUnroll * 4);
+  if (ok)
+    quantize_kernel<4><<<grid, kThreads, 0, s>>>(x, n, head, d_range, codes, d_meta, adopt_out,
+                                                 avg_div);
+  else
+    quantize_kernel<1><<<grid, kThreads, 0, s>>>(x, n, 0, d_range, codes, d_meta, adopt_out,
+                                                 avg_div);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+int pcclb_dequantize_u8(float *out, const uint8_t *codes, uint64_t n, const pcclb_qmeta *d_meta,
+                        uint32_t avg_div, void *stream) {
+  if (!d_meta || (n && (!out || !codes)) || avg_div < 1) return PCCLB_EINVAL;
+  if (n == 0) return PCCLB_OK;
+  cudaStream_t s = as_stream(stream);
+  uint64_t head;
+  bool ok = fc_vec_ok(out, codes, &head);
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * 4);
+  if (ok)
+    dequantize_kernel<4><<<grid, kThreads, 0, s>>>(out, codes, n, head, d_meta, avg_div);
+  else
+    dequantize_kernel<1><<<grid, kThreads, 0, s>>>(out, codes, n, 0, d_meta, avg_div);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint64_t n,
+                                const pcclb_qmeta *d_meta, int op, pcclb_range *d_next_range,
+                                void *stream) {
+  if (!d_meta || !valid_op(op) || (n && (!acc || !codes))) return PCCLB_EINVAL;
+  if (n == 0) return PCCLB_OK;
+  cudaStream_t s = as_stream(stream);
+  uint64_t head;
+  bool ok = fc_vec_ok(acc, codes, &head);
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * 4);
+#define PCCLB_DQA(OPC)                                                                      \
+  if (ok)                                                                                   \
+    dequant_acc_kernel<OPC, 4><<<grid, kThreads, 0, s>>>(acc, codes, n, head, d_meta,       \
+                                                         d_next_range);                     \
+  else                                                                                      \
+    dequant_acc_kernel<OPC, 1><<<grid, kThreads, 0, s>>>(acc, codes, n, 0, d_meta, d_next_range);
+  switch (op) {
+    case PCCLB_MAX:
+      PCCLB_DQA(PCCLB_MAX);
+      break;
+    case PCCLB_MIN:
+      PCCLB_DQA(PCCLB_MIN);
+      break;
+    default:
+      PCCLB_DQA(PCCLB_SUM);
+      break;
+  }
+#undef PCCLB_DQA
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+}  // extern "C"

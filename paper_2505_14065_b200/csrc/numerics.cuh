@@ -1,0 +1,224 @@
+// Element arithmetic that reproduces the reference's NumPy results bit for bit.
+//
+// The reference computes with NumPy ufuncs on x86 (collective.py:66-71,
+// :119-135, :479-482). Probed behaviour (NumPy 2.3.5, see DESIGN.md
+// §Numerics and tests/golden/edges.npz):
+//   * add/sub/mul/div: IEEE binary32/64 round-to-nearest, no contraction, no
+//     FTZ. A NaN operand propagates quieted (first operand wins); an invalid
+//     operation yields the x86 default NaN (0xffc00000 / 0xfff8000000000000),
+//     not the CUDA canonical 0x7fffffff.
+//   * np.maximum(a, b): a if a > b or a is NaN, else b  -> ties and a NaN b
+//     return b (the incoming operand); NaN returned unquieted.
+//   * np.minimum(a, b): a if a < b or a is NaN, else b.
+//   * rint: ties-to-even; f32 -> u8 cast of NaN gives 0 (cvttss2si path).
+// The library is compiled with -fmad=false -prec-div=true -ftz=false; the
+// explicit _rn intrinsics below keep that true regardless of flags.
+#pragma once
+
+#include <stdint.h>
+
+#include "pcclb200.h"
+
+namespace pcclb {
+
+template <typename T>
+struct FTraits;
+template <>
+struct FTraits<float> {
+  using U = uint32_t;
+  static constexpr U kQuiet = 0x00400000u;
+  static constexpr U kDefaultNaN = 0xffc00000u;
+  static __device__ __forceinline__ U bits(float x) { return __float_as_uint(x); }
+  static __device__ __forceinline__ float from(U u) { return __uint_as_float(u); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+};
+template <>
+struct FTraits<double> {
+  using U = unsigned long long;
+  static constexpr U kQuiet = 0x0008000000000000ull;
+  static constexpr U kDefaultNaN = 0xfff8000000000000ull;
+  static __device__ __forceinline__ U bits(double x) { return (U)__double_as_longlong(x); }
+  static __device__ __forceinline__ double from(U u) { return __longlong_as_double((long long)u); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+
+template <typename T>
+__device__ __forceinline__ bool is_nan(T x) {
+  return x != x;
+}
+
+template <typename T>
+__device__ __forceinline__ T quiet(T x) {
+  using F = FTraits<T>;
+  return F::from(F::bits(x) | F::kQuiet);
+}
+
+// NaN result of a binary x86 SSE operation: first NaN operand quieted, else
+// the default NaN (invalid operation).
+template <typename T>
+__device__ __noinline__ T x86_nan_result(T a, T b) {
+  if (is_nan(a)) return quiet(a);
+  if (is_nan(b)) return quiet(b);
+  return FTraits<T>::from(FTraits<T>::kDefaultNaN);
+}
+
+template <typename T>
+__device__ __forceinline__ T x86_add(T a, T b) {
+  T r = FTraits<T>::add(a, b);
+  if (__builtin_expect(is_nan(r), 0)) r = x86_nan_result(a, b);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T x86_sub(T a, T b) {
+  T r = FTraits<T>::sub(a, b);
+  if (__builtin_expect(is_nan(r), 0)) r = x86_nan_result(a, b);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T x86_mul(T a, T b) {
+  T r = FTraits<T>::mul(a, b);
+  if (__builtin_expect(is_nan(r), 0)) r = x86_nan_result(a, b);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T x86_div(T a, T b) {
+  T r = FTraits<T>::div(a, b);
+  if (__builtin_expect(is_nan(r), 0)) r = x86_nan_result(a, b);
+  return r;
+}
+// np.maximum / np.minimum (collective.py:69-70)
+template <typename T>
+__device__ __forceinline__ T np_maximum(T a, T b) {
+  return (a > b || is_nan(a)) ? a : b;
+}
+template <typename T>
+__device__ __forceinline__ T np_minimum(T a, T b) {
+  return (a < b || is_nan(a)) ? a : b;
+}
+
+// accumulate(local, incoming) for a reduce op code (AVG accumulates with add)
+template <int OP, typename T>
+__device__ __forceinline__ T reduce_op(T local, T incoming) {
+  if constexpr (OP == PCCLB_MAX) {
+    return np_maximum(local, incoming);
+  } else if constexpr (OP == PCCLB_MIN) {
+    return np_minimum(local, incoming);
+  } else {
+    return x86_add(local, incoming);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// quantization (collective.py:109-135)
+// ---------------------------------------------------------------------------
+// order-preserving key of a float (-0 sorts just below +0)
+__device__ __forceinline__ uint32_t fkey(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_decode(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
+
+struct QParams {
+  float mn;
+  float scale;
+};
+
+// (min, scale) from a span range: scale = (max - min) / 255f, 1 when 0.
+// Empty span -> (0, 1) (collective.py:115-116).
+__device__ __forceinline__ QParams qparams_from_range(const pcclb_range &r) {
+  QParams q;
+  if (!r.seen) {
+    q.mn = 0.0f;
+    q.scale = 1.0f;
+    return q;
+  }
+  float mn = fkey_decode(~r.kmin_inv);
+  float mx = fkey_decode(r.kmax);
+  float s = x86_div(x86_sub(mx, mn), 255.0f);
+  if (s == 0.0f) s = 1.0f;
+  q.mn = mn;
+  q.scale = s;
+  return q;
+}
+
+// q = u8(clip(rint((x - min) / scale), 0, 255)); NaN -> 0
+__device__ __forceinline__ uint32_t quant1(float x, float mn, float scale) {
+  float t = x86_div(x86_sub(x, mn), scale);
+  t = rintf(t);
+  if (is_nan(t)) return 0u;
+  t = fminf(fmaxf(t, 0.0f), 255.0f);
+  return (uint32_t)t;
+}
+
+// x = f32(q) * scale (RN) + min (RN), x86 NaN rules
+__device__ __forceinline__ float dequant1(uint32_t q, float mn, float scale) {
+  return x86_add(x86_mul((float)q, scale), mn);
+}
+
+// block-wide range accumulation helpers
+struct RangeAcc {
+  uint32_t kmin_inv = 0;
+  uint32_t kmax = 0;
+  uint32_t nonfinite = 0;
+  uint32_t seen = 0;
+  __device__ __forceinline__ void add(float x) {
+    uint32_t k = fkey(x);
+    kmin_inv = max(kmin_inv, ~k);
+    kmax = max(kmax, k);
+    nonfinite |= finite_f(x) ? 0u : 1u;
+    seen = 1u;
+  }
+};
+
+// reduce a RangeAcc over the block and fold it into *dst with atomics
+__device__ __forceinline__ void range_block_commit(RangeAcc a, pcclb_range *dst) {
+  __shared__ uint32_t s_inv[32], s_max[32], s_nf[32], s_seen[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a.kmin_inv = max(a.kmin_inv, __shfl_xor_sync(0xffffffffu, a.kmin_inv, o));
+    a.kmax = max(a.kmax, __shfl_xor_sync(0xffffffffu, a.kmax, o));
+    a.nonfinite |= __shfl_xor_sync(0xffffffffu, a.nonfinite, o);
+    a.seen |= __shfl_xor_sync(0xffffffffu, a.seen, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) {
+    s_inv[warp] = a.kmin_inv;
+    s_max[warp] = a.kmax;
+    s_nf[warp] = a.nonfinite;
+    s_seen[warp] = a.seen;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    RangeAcc b;
+    if (lane < nw) {
+      b.kmin_inv = s_inv[lane];
+      b.kmax = s_max[lane];
+      b.nonfinite = s_nf[lane];
+      b.seen = s_seen[lane];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      b.kmin_inv = max(b.kmin_inv, __shfl_xor_sync(0xffffffffu, b.kmin_inv, o));
+      b.kmax = max(b.kmax, __shfl_xor_sync(0xffffffffu, b.kmax, o));
+      b.nonfinite |= __shfl_xor_sync(0xffffffffu, b.nonfinite, o);
+      b.seen |= __shfl_xor_sync(0xffffffffu, b.seen, o);
+    }
+    if (lane == 0 && b.seen) {
+      atomicMax(&dst->kmin_inv, b.kmin_inv);
+      atomicMax(&dst->kmax, b.kmax);
+      if (b.nonfinite) atomicOr(&dst->nonfinite, 1u);
+      atomicOr(&dst->seen, 1u);
+    }
+  }
+}
+
+}  // namespace pcclb

@@ -1,0 +1,736 @@
+// Intra-box ring all-reduce over NVLink: one process per GPU, one engine per
+// process (SURVEY §8(b) engine seam; reference run_all_reduce,
+// collective.py:489-576).
+//
+// Transport. Every rank cudaMalloc's one workspace, exports it with
+// cudaIpcGetMemHandle and maps every peer's workspace
+// (cudaIpcOpenMemHandle): kernels then load peer memory directly over
+// NVLink 5 / NVSwitch. No NCCL collective is used -- ncclAllReduce / NVLS
+// reduce in a different order and would not be bit-exact.
+//
+// Workspace layout (identical offsets on every rank for a given N):
+//   [0, 16 KiB)       Signal: barrier arrivals / abort tokens written by peers,
+//                     quantization metas, range slots, status word
+//   in   [N elems]    copy of the caller's input = the backup (collective.py:501-504)
+//   res  [n_c elems]  plain: fold result of the owned chunk
+//   codes0/1 [n_c B]  quantized: wire codes of reduce steps (double-buffered)
+//   codesF   [n_c B]  quantized: owned chunk's final codes for the gather
+//
+// Plain schedule (2 barriers). Each chunk's fold chain x_c, x_{c+1}, ..., x_{c-1}
+// (SURVEY §0 finding 2) is computed by the chunk's owner (rank c-1, as in the
+// reference) in ONE kernel that loads the W inputs of an element -- W-1 of
+// them from peers over NVLink -- folds them in ring order, divides (AVG) and
+// stores. NVLink ingress per rank is (W-1)*n_c for the fold plus (W-1)*n_c for
+// the gather: the ring's 2(W-1)/W*N, in one step instead of W-1.
+//   copy-in  buf -> in                 (local)
+//   barrier 0
+//   fold     owned chunk <- fold(peers' in)  -> res, buf[owned]
+//   barrier 1
+//   gather   buf[c'] <- owner(c').res   for the W-1 other chunks
+// Quantized schedule (W barriers): the fold order includes a quantize/
+// dequantize round trip whose range spans the whole partial sum, so hops
+// cannot be fused; it runs the reference's ring steps, sending u8 codes:
+//   copy-in; range(tx_0)
+//   step s: codes[s%2] <- Q(buf[tx_s]); barrier s;
+//           buf[rx_s] <- buf[rx_s] (+) D(pred.codes[s%2]) (+ range of result)
+//   prologue: codesF <- Q(buf[own]); buf[own] <- D(codesF)/W; barrier W-1
+//   gather: buf[c'] <- D(owner(c').codesF)/W
+//
+// Synchronisation. A barrier is one tiny kernel: thread j stores the token
+// (attempt << 8 | index) into peer j's arrival slot with st.release.sys and
+// thread 0 polls its own slots with ld.acquire.sys. It aborts instead of
+// arriving when the host abort word (set by the control plane, like the
+// reference's abort_event, client.py:196-204) is raised, when a fault is
+// injected (reference fault_hook, collective.py:268-272), when a quantized
+// span was non-finite, when a peer posted an abort token for this attempt,
+// or on timeout; it then posts its own abort token to every peer. Later
+// kernels of the op see the status word and skip. The host reads the status
+// at the end and restores the caller's buffer from `in` (collective.py:568-574).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "ew_ops.cuh"
+#include "numerics.cuh"
+
+namespace pcclb {
+
+constexpr int kIpcMaxWorld = 64;
+constexpr uint64_t kSignalBytes = 16384;
+constexpr int kIpcThreads = 512;
+
+struct Signal {
+  uint64_t arrive[kIpcMaxWorld];     // written by peer j: its latest barrier token
+  uint64_t abort_tok[kIpcMaxWorld];  // written by peer j: attempt it aborted
+  pcclb_qmeta meta[2];               // reduce-step metas (by step parity)
+  pcclb_qmeta meta_final;            // owned chunk's gather meta
+  uint32_t status;                   // this rank's op status (0 = ok)
+  uint32_t pad;
+  pcclb_range range[kIpcMaxWorld + 1];  // range of the span sent at step s
+};
+static_assert(sizeof(Signal) <= kSignalBytes, "signal area too small");
+
+struct HostFlags {
+  volatile uint32_t abort;  // set by the control plane
+  uint32_t pad[15];
+};
+
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct BarrierArgs {
+  Signal *mine;
+  Signal *peer[kIpcMaxWorld];
+  const HostFlags *host;   // device view of host-mapped flags
+  const pcclb_range *check_range;  // nullable: abort if non-finite
+  uint64_t token;
+  uint64_t attempt;
+  uint64_t timeout_ns;
+  uint32_t rank, world;
+  uint32_t fault;  // 1: inject a local fault here
+};
+
+__global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__ BarrierArgs a) {
+  __shared__ uint32_t s_verdict;
+  const uint32_t t = threadIdx.x;
+  Signal *me = a.mine;
+  if (t == 0) {
+    uint32_t v = *(volatile uint32_t *)&me->status;
+    if (v == 0) {
+      if (a.fault) v = PCCLB_EIO;
+      else if (a.host->abort) v = PCCLB_EABORTED;
+      else if (a.check_range && a.check_range->nonfinite) v = PCCLB_ENONFINITE;
+    }
+    s_verdict = v;
+  }
+  __syncthreads();
+  uint32_t v = s_verdict;
+  if (v != 0) {
+    // abort instead of arriving (keeps peers from passing this barrier)
+    if (t < a.world && t != a.rank) st_release_sys(&a.peer[t]->abort_tok[a.rank], a.attempt);
+    if (t == 0) *(volatile uint32_t *)&me->status = v;
+    return;
+  }
+  __threadfence_system();
+  if (t < a.world && t != a.rank) st_release_sys(&a.peer[t]->arrive[a.rank], a.token);
+  if (t != 0) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t verdict = 0;
+  for (;;) {
+    bool all = true;
+    for (uint32_t j = 0; j < a.world; ++j) {
+      if (j == a.rank) continue;
+      if (ld_acquire_sys(&me->arrive[j]) < a.token) all = false;
+      if (ld_acquire_sys(&me->abort_tok[j]) == a.attempt) verdict = PCCLB_EABORTED;
+    }
+    if (verdict) break;
+    if (all) break;
+    if (a.host->abort) {
+      verdict = PCCLB_EABORTED;
+      break;
+    }
+    if (globaltimer() - t0 > a.timeout_ns) {
+      verdict = PCCLB_ETIMEOUT;
+      break;
+    }
+    __nanosleep(64);
+  }
+  if (verdict) {
+    for (uint32_t j = 0; j < a.world; ++j)
+      if (j != a.rank) st_release_sys(&a.peer[j]->abort_tok[a.rank], a.attempt);
+    *(volatile uint32_t *)&me->status = verdict;
+  }
+}
+
+// peel16 usable on device too
+template <typename T>
+__device__ __forceinline__ uint64_t dpeel16(const void *p) {
+  uintptr_t x = reinterpret_cast<uintptr_t>(p);
+  return (uint64_t)(((16 - (x & 15)) & 15) / sizeof(T));
+}
+
+__device__ __forceinline__ bool op_failed(const Signal *me) {
+  return *(volatile const uint32_t *)&me->status != 0;
+}
+
+// ---------------------------------------------------------------------------
+// plain fold: owned chunk from W inputs (W-1 remote), chain order
+// ---------------------------------------------------------------------------
+template <typename T>
+struct FoldArgs {
+  const T *src[kIpcMaxWorld];  // src[k] = input of ring position (c + k) at chunk c
+  T *dst0;                     // res
+  T *dst1;                     // caller buffer at chunk c
+  const Signal *mine;
+  uint64_t n;
+  uint32_t w;
+  uint32_t avg;
+};
+
+template <typename T, int OP, int VEC>
+__global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
+  if (op_failed(a.mine)) return;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t w = a.w;
+  auto fin = [&](T v) { return a.avg ? x86_div(v, (T)a.avg) : v; };
+  auto one = [&](uint64_t i) {
+    T acc = a.src[0][i];
+    for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.src[k][i], acc);
+    acc = fin(acc);
+    a.dst0[i] = acc;
+    a.dst1[i] = acc;
+  };
+  if constexpr (VEC == 1) {
+    for (uint64_t i = tid; i < a.n; i += nth) one(i);
+  } else {
+    constexpr int N = Pack16<T>::N;
+    uint64_t head = dpeel16<T>(a.dst1);
+    if (head > a.n) head = a.n;
+    if (tid < head) one(tid);
+    const uint64_t nv = (a.n - head) / N;
+    for (uint64_t v = tid; v < nv; v += nth) {
+      const uint64_t i = head + v * N;
+      Pack16<T> acc = ld16(a.src[0] + i);
+#pragma unroll 8
+      for (uint32_t k = 1; k < w; ++k) {
+        Pack16<T> x = ld16(a.src[k] + i);
+#pragma unroll
+        for (int e = 0; e < N; ++e) acc.e[e] = reduce_op<OP>(x.e[e], acc.e[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < N; ++e) acc.e[e] = fin(acc.e[e]);
+      st16(a.dst0 + i, acc);
+      st16(a.dst1 + i, acc);
+    }
+    const uint64_t t0 = head + nv * N;
+    if (tid < a.n - t0) one(t0 + tid);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// gather: W-1 chunk copies (grid.y = job), plain (verbatim) or quantized (dequant)
+// ---------------------------------------------------------------------------
+struct GatherArgs {
+  const void *src[kIpcMaxWorld];       // plain: owner's res; quantized: owner's codesF
+  const pcclb_qmeta *meta[kIpcMaxWorld];  // quantized: owner's meta_final
+  void *dst[kIpcMaxWorld];             // caller buffer at that chunk
+  uint64_t n[kIpcMaxWorld];
+  const Signal *mine;
+  uint32_t avg;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __grid_constant__ GatherArgs a) {
+  if (op_failed(a.mine)) return;
+  const uint32_t j = blockIdx.y;
+  const T *src = static_cast<const T *>(a.src[j]);
+  T *dst = static_cast<T *>(a.dst[j]);
+  const uint64_t n = a.n[j];
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int N = Pack16<T>::N;
+  uint64_t head = dpeel16<T>(dst);
+  if (head > n) head = n;
+  const bool vec = dpeel16<T>(src) == head;
+  if (!vec) {
+    for (uint64_t i = tid; i < n; i += nth) dst[i] = src[i];
+    return;
+  }
+  if (tid < head) dst[tid] = src[tid];
+  const uint64_t nv = (n - head) / N;
+  uint64_t v = tid;
+  for (; v + 3 * nth < nv; v += 4 * nth) {
+    Pack16<T> x0 = ld16(src + head + v * N), x1 = ld16(src + head + (v + nth) * N);
+    Pack16<T> x2 = ld16(src + head + (v + 2 * nth) * N), x3 = ld16(src + head + (v + 3 * nth) * N);
+    st16(dst + head + v * N, x0);
+    st16(dst + head + (v + nth) * N, x1);
+    st16(dst + head + (v + 2 * nth) * N, x2);
+    st16(dst + head + (v + 3 * nth) * N, x3);
+  }
+  for (; v < nv; v += nth) st16(dst + head + v * N, ld16(src + head + v * N));
+  const uint64_t t0 = head + nv * N;
+  if (tid < n - t0) dst[t0 + tid] = src[t0 + tid];
+}
+
+__global__ void __launch_bounds__(kIpcThreads) ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a) {
+  if (op_failed(a.mine)) return;
+  const uint32_t j = blockIdx.y;
+  const uint64_t n = a.n[j];
+  float *dst = static_cast<float *>(a.dst[j]);
+  const uint8_t *codes = static_cast<const uint8_t *>(a.src[j]);
+  const pcclb_qmeta m = *a.meta[j];
+  DequantF f{dst, codes, m.min_val, m.scale, (float)a.avg, a.avg > 1};
+  uint64_t head = dpeel16<float>(dst);
+  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
+    ew_loop<4, 2>(n, head, f);
+  else
+    ew_loop<1, 1>(n, 0, f);
+}
+
+// ---------------------------------------------------------------------------
+// quantized step kernels (skip after a failure)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kIpcThreads)
+    ipc_range_kernel(const float *x, uint64_t n, pcclb_range *out, const Signal *mine) {
+  if (op_failed(mine)) return;
+  RangeF f{x, RangeAcc()};
+  uint64_t head = dpeel16<float>(x);
+  ew_loop<4, 4>(n, head, f);
+  range_block_commit(f.acc, out);
+}
+
+__global__ void __launch_bounds__(kIpcThreads)
+    ipc_quantize_kernel(const float *x, uint64_t n, const pcclb_range *range, uint8_t *codes,
+                        pcclb_qmeta *meta, float *adopt, uint32_t avg, const Signal *mine) {
+  if (op_failed(mine)) return;
+  QParams qp = qparams_from_range(*range);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta->min_val = qp.mn;
+    meta->scale = qp.scale;
+  }
+  QuantF f{x, codes, adopt, qp, (float)avg, avg > 1};
+  uint64_t head = dpeel16<float>(x);
+  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
+    ew_loop<4, 4>(n, head, f);
+  else
+    ew_loop<1, 1>(n, 0, f);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kIpcThreads)
+    ipc_dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, const pcclb_qmeta *meta,
+                           pcclb_range *next, const Signal *mine) {
+  if (op_failed(mine)) return;
+  const pcclb_qmeta m = *meta;  // peer memory
+  DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc()};
+  uint64_t head = dpeel16<float>(acc);
+  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
+    ew_loop<4, 4>(n, head, f);
+  else
+    ew_loop<1, 1>(n, 0, f);
+  range_block_commit(f.r, next);
+}
+
+}  // namespace pcclb
+
+using namespace pcclb;
+
+struct pcclb_ring {
+  int device;
+  uint32_t rank, world;
+  uint64_t capacity;
+  char *ws;                        // own workspace
+  char *peer_ws[kIpcMaxWorld];     // mapped (own rank: ws)
+  bool imported[kIpcMaxWorld];
+  HostFlags *host;                 // host-mapped
+  HostFlags *host_dev;             // device alias
+  uint32_t *status_host;           // pinned status readback
+  uint64_t last_n;
+  int last_dtype;
+  bool have_backup;
+};
+
+static Signal *sig_of(char *base) { return reinterpret_cast<Signal *>(base); }
+
+namespace {
+
+struct Layout {
+  uint64_t in, res, codes0, codes1, codesF, end;
+};
+
+// Chunk-local buffers keep the chunk's sub-16-byte alignment (floats) or
+// sub-4-byte alignment (codes), so vector bodies line up with the caller's
+// buffer at the same element offset.
+uint64_t res_off(const Layout &L, uint64_t lo, size_t esz) { return L.res + (lo * esz) % 16; }
+uint64_t codes_at(uint64_t off, uint64_t lo) { return off + lo % 4; }
+
+Layout layout_for(uint64_t n, uint32_t w, size_t esz, bool quant) {
+  Layout L{};
+  const uint64_t nc = (n + w - 1) / w;
+  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  L.in = kSignalBytes;
+  uint64_t off = up(L.in + n * esz);
+  if (!quant) {
+    L.res = off;
+    off = up(off + nc * esz + 16);
+  } else {
+    L.codes0 = off;
+    off = up(off + nc + 4);
+    L.codes1 = off;
+    off = up(off + nc + 4);
+    L.codesF = off;
+    off = up(off + nc + 4);
+  }
+  L.end = off;
+  return L;
+}
+
+int launch_barrier(pcclb_ring *r, uint64_t attempt, uint32_t index, int fault_at,
+                   const pcclb_range *check, uint64_t timeout_ns, cudaStream_t s) {
+  BarrierArgs a{};
+  a.mine = sig_of(r->ws);
+  for (uint32_t j = 0; j < r->world; ++j) a.peer[j] = sig_of(r->peer_ws[j]);
+  a.host = r->host_dev;
+  a.check_range = check;
+  a.token = (attempt << 8) | index;
+  a.attempt = attempt;
+  a.timeout_ns = timeout_ns;
+  a.rank = r->rank;
+  a.world = r->world;
+  a.fault = (fault_at >= 0 && (uint32_t)fault_at == index) ? 1u : 0u;
+  ipc_barrier_kernel<<<1, 64, 0, s>>>(a);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
+  return grid_for(n_vec, kIpcThreads, ctas_per_sm);
+}
+
+template <typename T>
+int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt, int fault_at,
+                    uint64_t timeout_ns, cudaStream_t s) {
+  const uint32_t w = r->world, rank = r->rank;
+  const Layout L = layout_for(n, w, sizeof(T), false);
+  uint64_t lo[2 * kIpcMaxWorld];
+  pcclb_chunk_bounds(n, w, lo);  // lo[2c], lo[2c+1]
+  const uint32_t own = (rank + 1) % w;  // collective.py:538
+  const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
+  Signal *me = sig_of(r->ws);
+  // copy-in: the caller's bytes become the backup and the peers' fold input
+  PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  int rc = launch_barrier(r, attempt, 0, fault_at, nullptr, timeout_ns, s);
+  if (rc) return rc;
+  if (own_n) {
+    FoldArgs<T> f{};
+    for (uint32_t k = 0; k < w; ++k)
+      f.src[k] = reinterpret_cast<const T *>(r->peer_ws[(own + k) % w] + L.in) + own_lo;
+    f.dst0 = reinterpret_cast<T *>(r->ws + res_off(L, own_lo, sizeof(T)));
+    f.dst1 = buf + own_lo;
+    f.mine = me;
+    f.n = own_n;
+    f.w = w;
+    f.avg = (op == PCCLB_AVG) ? w : 0;
+    const unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
+    // peers' inputs and res share the chunk's sub-16-byte offset; buf must too
+    const bool vec = peel16<T>(f.dst1) == peel16<T>(f.src[0]) && peel16<T>(f.dst0) == peel16<T>(f.src[0]);
+#define PCCLB_IPC_FOLD(OPC)                                                             \
+  if (vec)                                                                              \
+    ipc_fold_kernel<T, OPC, 16 / sizeof(T)><<<grid, kIpcThreads, 0, s>>>(f);            \
+  else                                                                                  \
+    ipc_fold_kernel<T, OPC, 1><<<grid, kIpcThreads, 0, s>>>(f);
+    switch (op) {
+      case PCCLB_MAX:
+        PCCLB_IPC_FOLD(PCCLB_MAX);
+        break;
+      case PCCLB_MIN:
+        PCCLB_IPC_FOLD(PCCLB_MIN);
+        break;
+      default:
+        PCCLB_IPC_FOLD(PCCLB_SUM);
+        break;
+    }
+#undef PCCLB_IPC_FOLD
+    PCCLB_LAUNCH_CHECK();
+  }
+  rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
+  if (rc) return rc;
+  GatherArgs g{};
+  g.mine = me;
+  uint32_t jobs = 0;
+  uint64_t maxn = 0;
+  for (uint32_t c = 0; c < w; ++c) {
+    if (c == own) continue;
+    const uint64_t cn = lo[2 * c + 1] - lo[2 * c];
+    if (!cn) continue;
+    const uint32_t owner = (c + w - 1) % w;
+    g.src[jobs] = r->peer_ws[owner] + res_off(L, lo[2 * c], sizeof(T));
+    g.dst[jobs] = buf + lo[2 * c];
+    g.n[jobs] = cn;
+    maxn = cn > maxn ? cn : maxn;
+    ++jobs;
+  }
+  if (jobs) {
+    unsigned per = ipc_grid(maxn / Pack16<T>::N + 1, 4);
+    per = (per + jobs - 1) / jobs;
+    if (per < 1) per = 1;
+    ipc_gather_plain_kernel<T><<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
+    PCCLB_LAUNCH_CHECK();
+  }
+  return PCCLB_OK;
+}
+
+int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t attempt, int fault_at,
+                    uint64_t timeout_ns, cudaStream_t s) {
+  const uint32_t w = r->world, rank = r->rank;
+  const Layout L = layout_for(n, w, 4, true);
+  uint64_t lo[2 * kIpcMaxWorld];
+  pcclb_chunk_bounds(n, w, lo);
+  Signal *me = sig_of(r->ws);
+  const uint32_t pred = (rank + w - 1) % w;
+  Signal *pred_sig = sig_of(r->peer_ws[pred]);
+  PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  // range slots reset
+  PCCLB_CUDA(cudaMemsetAsync(me->range, 0, sizeof(pcclb_range) * (w + 1), s));
+  auto span = [&](uint32_t c, uint64_t &a, uint64_t &len) {
+    a = lo[2 * c];
+    len = lo[2 * c + 1] - lo[2 * c];
+  };
+  uint64_t a0, n0;
+  span(rank % w, a0, n0);  // step-0 tx chunk = rank (collective.py:522)
+  if (n0) {
+    ipc_range_kernel<<<ipc_grid(n0 / 4 + 1), kIpcThreads, 0, s>>>(buf + a0, n0, &me->range[0], me);
+    PCCLB_LAUNCH_CHECK();
+  }
+  int rc;
+  for (uint32_t step = 0; step + 1 < w; ++step) {
+    const uint32_t tx = (rank + w - step % w) % w;         // (rank - step) mod w
+    const uint32_t rx = (rank + 2 * w - step - 1) % w;      // (rank - step - 1) mod w
+    uint64_t ta, tn, ra, rn;
+    span(tx, ta, tn);
+    span(rx, ra, rn);
+    const uint64_t codes_off = (step & 1) ? L.codes1 : L.codes0;
+    // quantize what we send (its range was produced by the previous step)
+    ipc_quantize_kernel<<<ipc_grid(tn / 4 + 1), kIpcThreads, 0, s>>>(
+        buf + ta, tn, &me->range[step], reinterpret_cast<uint8_t *>(r->ws + codes_at(codes_off, ta)),
+        &me->meta[step & 1], nullptr, 1, me);
+    PCCLB_LAUNCH_CHECK();
+    rc = launch_barrier(r, attempt, step, fault_at, &me->range[step], timeout_ns, s);
+    if (rc) return rc;
+    if (rn) {
+      const uint8_t *codes = reinterpret_cast<const uint8_t *>(r->peer_ws[pred] + codes_at(codes_off, ra));
+      const pcclb_qmeta *meta = &pred_sig->meta[step & 1];
+      const unsigned grid = ipc_grid(rn / 4 + 1);
+      switch (op) {
+        case PCCLB_MAX:
+          ipc_dequant_acc_kernel<PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          break;
+        case PCCLB_MIN:
+          ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          break;
+        default:
+          ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          break;
+      }
+      PCCLB_LAUNCH_CHECK();
+    }
+  }
+  // gather prologue: owner adopts D(Q(own)) (collective.py:538-551), fused with AVG
+  const uint32_t own = (rank + 1) % w;
+  uint64_t oa, on;
+  span(own, oa, on);
+  const uint32_t avg = (op == PCCLB_AVG) ? w : 1;
+  ipc_quantize_kernel<<<ipc_grid(on / 4 + 1), kIpcThreads, 0, s>>>(
+      buf + oa, on, &me->range[w - 1], reinterpret_cast<uint8_t *>(r->ws + codes_at(L.codesF, oa)),
+      &me->meta_final, buf + oa, avg, me);
+  PCCLB_LAUNCH_CHECK();
+  rc = launch_barrier(r, attempt, w - 1, fault_at, &me->range[w - 1], timeout_ns, s);
+  if (rc) return rc;
+  GatherArgs g{};
+  g.mine = me;
+  g.avg = avg;
+  uint32_t jobs = 0;
+  uint64_t maxn = 0;
+  for (uint32_t c = 0; c < w; ++c) {
+    if (c == own) continue;
+    uint64_t ca, cn;
+    span(c, ca, cn);
+    if (!cn) continue;
+    const uint32_t owner = (c + w - 1) % w;
+    g.src[jobs] = r->peer_ws[owner] + codes_at(L.codesF, ca);
+    g.meta[jobs] = &sig_of(r->peer_ws[owner])->meta_final;
+    g.dst[jobs] = buf + ca;
+    g.n[jobs] = cn;
+    maxn = cn > maxn ? cn : maxn;
+    ++jobs;
+  }
+  if (jobs) {
+    unsigned per = ipc_grid(maxn / 4 + 1, 4);
+    per = (per + jobs - 1) / jobs;
+    if (per < 1) per = 1;
+    ipc_gather_quant_kernel<<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
+    PCCLB_LAUNCH_CHECK();
+  }
+  return PCCLB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capacity_bytes,
+                      pcclb_ring **out) {
+  if (!out || world < 1 || world > (uint32_t)kIpcMaxWorld || rank >= world) return PCCLB_EINVAL;
+  *out = nullptr;
+  PCCLB_CUDA(cudaSetDevice(device));
+  pcclb_ring *r = new (std::nothrow) pcclb_ring();
+  if (!r) return PCCLB_ENOMEM;
+  std::memset(r, 0, sizeof(*r));
+  r->device = device;
+  r->rank = rank;
+  r->world = world;
+  r->capacity = capacity_bytes < kSignalBytes + 4096 ? kSignalBytes + 4096 : capacity_bytes;
+  cudaError_t e = cudaMalloc(&r->ws, r->capacity);
+  if (e != cudaSuccess) {
+    delete r;
+    return cuda_status(e);
+  }
+  e = cudaMemset(r->ws, 0, kSignalBytes);
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->host, sizeof(HostFlags), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->host_dev, r->host, 0);
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, 64, cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    pcclb_ring_destroy(r);
+    return cuda_status(e);
+  }
+  std::memset((void *)r->host, 0, sizeof(HostFlags));
+  r->peer_ws[rank] = r->ws;
+  r->imported[rank] = true;
+  *out = r;
+  return PCCLB_OK;
+}
+
+int pcclb_ring_export(pcclb_ring *r, void *handle64_out) {
+  if (!r || !handle64_out) return PCCLB_EINVAL;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  cudaIpcMemHandle_t h;
+  PCCLB_CUDA(cudaIpcGetMemHandle(&h, r->ws));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  std::memcpy(handle64_out, &h, 64);
+  return PCCLB_OK;
+}
+
+int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle64) {
+  if (!r || !handle64 || peer >= r->world) return PCCLB_EINVAL;
+  if (peer == r->rank) return PCCLB_OK;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  if (r->imported[peer]) {
+    PCCLB_CUDA(cudaIpcCloseMemHandle(r->peer_ws[peer]));
+    r->imported[peer] = false;
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  void *p = nullptr;
+  PCCLB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  r->peer_ws[peer] = static_cast<char *>(p);
+  r->imported[peer] = true;
+  return PCCLB_OK;
+}
+
+volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r) { return r ? &r->host->abort : nullptr; }
+
+uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize) {
+  if (!r || !valid_dtype(dtype)) return 0;
+  // largest n whose layout fits (layout is monotone in n)
+  const size_t esz = dtype_size(dtype);
+  uint64_t lo = 0, hi = r->capacity / esz + 1;
+  while (lo + 1 < hi) {
+    uint64_t mid = lo + (hi - lo) / 2;
+    if (layout_for(mid, r->world, esz, quantize != 0).end <= r->capacity) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op, int quantize,
+                         uint64_t attempt, int fault_at, double timeout_s, pcclb_stats *out_stats,
+                         void *stream) {
+  if (!r || !valid_dtype(dtype) || !valid_op(op) || (n && !d_buf)) return PCCLB_EINVAL;
+  if (quantize && dtype != PCCLB_F32) return PCCLB_EINVAL;  // client.py:818-819
+  if (attempt == 0 || attempt >= (1ull << 55)) return PCCLB_EINVAL;
+  for (uint32_t j = 0; j < r->world; ++j)
+    if (!r->imported[j]) return PCCLB_EINVAL;
+  const size_t esz = dtype_size(dtype);
+  if (layout_for(n, r->world, esz, quantize != 0).end > r->capacity) return PCCLB_ENOMEM;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  cudaStream_t s = as_stream(stream);
+  const uint32_t w = r->world;
+  if (out_stats) {
+    // algorithmic payload per peer: 2(W-1)/W * N * elem (test_ring_engine.py:99-108)
+    uint64_t lo[2 * kIpcMaxWorld];
+    pcclb_chunk_bounds(n, w, lo);
+    uint64_t tx = 0;
+    const uint64_t ebytes = quantize ? 1 : esz;
+    for (uint32_t step = 0; step + 1 < w; ++step) {
+      uint32_t c = (r->rank + w - step % w) % w;
+      tx += (lo[2 * c + 1] - lo[2 * c]) * ebytes;
+    }
+    uint32_t cur = (r->rank + 1) % w;
+    for (uint32_t step = 0; step + 1 < w; ++step) {
+      tx += (lo[2 * cur + 1] - lo[2 * cur]) * ebytes;
+      cur = (cur + w - 1) % w;
+    }
+    out_stats->tx_payload_bytes = tx;
+    out_stats->rx_payload_bytes = tx;
+  }
+  r->last_n = n;
+  r->last_dtype = dtype;
+  r->have_backup = false;
+  if (w == 1) {  // client.py:896-900
+    int rc = pcclb_finalize(d_buf, n, dtype, op, 1, stream);
+    if (rc) return rc;
+    PCCLB_CUDA(cudaStreamSynchronize(s));
+    return PCCLB_OK;
+  }
+  Signal *me = sig_of(r->ws);
+  PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
+  const uint64_t timeout_ns = (uint64_t)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
+  int rc;
+  if (quantize)
+    rc = quant_allreduce(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+  else if (dtype == PCCLB_F32)
+    rc = plain_allreduce<float>(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+  else
+    rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+  if (rc) return rc;
+  r->have_backup = true;
+  PCCLB_CUDA(cudaMemcpyAsync(r->status_host, &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCCLB_CUDA(cudaStreamSynchronize(s));
+  const uint32_t st = *r->status_host;
+  if (st == 0) return PCCLB_OK;
+  // restore the caller's bytes (collective.py:568-574)
+  PCCLB_CUDA(cudaMemcpyAsync(d_buf, r->ws + kSignalBytes, n * esz, cudaMemcpyDeviceToDevice, s));
+  PCCLB_CUDA(cudaStreamSynchronize(s));
+  return (int)st;
+}
+
+int pcclb_ring_restore(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, void *stream) {
+  if (!r || !d_buf || !r->have_backup || n != r->last_n || dtype != r->last_dtype) return PCCLB_EINVAL;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  cudaStream_t s = as_stream(stream);
+  PCCLB_CUDA(cudaMemcpyAsync(d_buf, r->ws + kSignalBytes, n * dtype_size(dtype), cudaMemcpyDeviceToDevice, s));
+  PCCLB_CUDA(cudaStreamSynchronize(s));
+  return PCCLB_OK;
+}
+
+void pcclb_ring_destroy(pcclb_ring *r) {
+  if (!r) return;
+  cudaSetDevice(r->device);
+  cudaDeviceSynchronize();
+  for (uint32_t j = 0; j < r->world; ++j)
+    if (j != r->rank && r->imported[j] && r->peer_ws[j]) cudaIpcCloseMemHandle(r->peer_ws[j]);
+  if (r->ws) cudaFree(r->ws);
+  if (r->host) cudaFreeHost((void *)r->host);
+  if (r->status_host) cudaFreeHost(r->status_host);
+  delete r;
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+"""One-process-per-GPU ring all-reduce over NVLink (csrc/ring_ipc.cu).
+
+``DeviceRing`` is the engine seam of the reference's ``run_all_reduce``
+(collective.py:489-576): it runs one attempt of a tagged all-reduce over the
+committed ring order on a CUDA tensor, in place, and raises
+``CollectiveAborted`` after restoring the caller's bytes when the attempt is
+aborted (host abort word, peer abort, timeout, injected fault, non-finite
+quantized span).
+
+torch.distributed is used only as plumbing: once per workspace it exchanges
+the 64-byte CUDA IPC handles. The data path never calls NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native
+from ._native import Stats, check, lib
+from .collective import DTYPE_CODE, CollectiveAborted, ReduceOp, UsageError
+
+_STATUS_REASON = {
+    _native.PCCLB_EABORTED: ("abort signaled", "master"),
+    _native.PCCLB_ETIMEOUT: ("io failure: peer timeout", "io"),
+    _native.PCCLB_EIO: ("io failure: injected fault", "io"),
+    _native.PCCLB_ENONFINITE: ("non-finite values cannot be quantized", "io"),
+}
+
+
+@dataclass
+class ReduceStats:
+    tx_payload_bytes: int
+    rx_payload_bytes: int
+
+
+def exchange_bytes(payload: bytes, group=None) -> list[bytes]:
+    """all_gather of a small byte string over the process group."""
+    out: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, payload, group=group)
+    return out
+
+
+class DeviceRing:
+    """Ring engine for this process's GPU.
+
+    ``ring`` lists global ranks in ring order (the master's committed ring,
+    client.py:902); this rank's ring position is its index in it.
+    """
+
+    def __init__(self, group=None, ring: list[int] | None = None, device=None,
+                 capacity_bytes: int = 64 << 20, timeout_s: float = 60.0):
+        if not dist.is_initialized():
+            raise UsageError("torch.distributed must be initialized")
+        self.group = group
+        world = dist.get_world_size(group)
+        me = dist.get_rank(group)
+        self.ring = list(ring) if ring is not None else list(range(world))
+        if sorted(self.ring) != list(range(world)):
+            raise UsageError("ring must be a permutation of the group's ranks")
+        self.position = self.ring.index(me)
+        self.world = world
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.timeout_s = timeout_s
+        self._attempt = 0
+        self._handle = None
+        self._capacity = 0
+        self._create(capacity_bytes)
+
+    # -- workspace lifecycle (collective: every rank calls in the same order) --
+    def _create(self, capacity_bytes: int) -> None:
+        self._destroy()
+        h = ctypes.c_void_p()
+        check(
+            lib().pcclb_ring_create(self.device.index, self.position, self.world, capacity_bytes, ctypes.byref(h)),
+            "ring_create",
+        )
+        self._handle = h
+        self._capacity = capacity_bytes
+        mine = ctypes.create_string_buffer(64)
+        check(lib().pcclb_ring_export(h, mine), "ring_export")
+        handles = exchange_bytes(bytes(mine.raw), self.group)  # indexed by group rank
+        for pos, grank in enumerate(self.ring):
+            if pos == self.position:
+                continue
+            buf = ctypes.create_string_buffer(handles[grank], 64)
+            check(lib().pcclb_ring_import(h, pos, buf), f"ring_import(peer {pos})")
+        self._abort = lib().pcclb_ring_abort_word(h)
+
+    def _destroy(self) -> None:
+        if self._handle is not None:
+            lib().pcclb_ring_destroy(self._handle)
+            self._handle = None
+
+    def close(self) -> None:
+        self._destroy()
+
+    def __del__(self):
+        try:
+            self._destroy()
+        except Exception:
+            pass
+
+    def ensure_capacity(self, n: int, dtype: torch.dtype, quantize: bool) -> None:
+        code = DTYPE_CODE[dtype]
+        if lib().pcclb_ring_capacity(self._handle, code, int(quantize)) >= n:
+            return
+        esz = torch.tensor([], dtype=dtype).element_size()
+        need = 16384 + n * esz + 4 * ((n + self.world - 1) // self.world) * max(esz, 1) + 4096
+        self._create(int(need * 1.05))
+
+    # -- control-plane hooks --
+    def signal_abort(self) -> None:
+        """Raise the host abort word (the tag box abort_event, client.py:196-204)."""
+        self._abort[0] = 1
+
+    def reset_abort(self) -> None:
+        """Clear the abort word for a new attempt (box.reset_for_attempt)."""
+        self._abort[0] = 0
+
+    # -- the op --
+    def run_all_reduce(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,
+                       fault_at: int = -1, stream: torch.cuda.Stream | None = None) -> ReduceStats:
+        op = ReduceOp.parse(op)
+        if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1 or not buffer.is_contiguous():
+            raise UsageError("buffer must be a one-dimensional contiguous tensor")
+        if buffer.device != self.device:
+            raise UsageError(f"buffer must live on {self.device}")
+        if buffer.dtype not in DTYPE_CODE:
+            raise UsageError(f"unsupported dtype {buffer.dtype}")
+        if quantize and buffer.dtype != torch.float32:
+            raise UsageError("quantization requires float32 buffers")
+        n = buffer.numel()
+        self.ensure_capacity(n, buffer.dtype, quantize)
+        self._attempt += 1
+        stats = Stats()
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        rc = lib().pcclb_ring_allreduce(
+            self._handle, buffer.data_ptr(), n, DTYPE_CODE[buffer.dtype], op.code, int(quantize),
+            self._attempt, fault_at, self.timeout_s, ctypes.byref(stats), s,
+        )
+        if rc in _STATUS_REASON:
+            reason, source = _STATUS_REASON[rc]
+            raise CollectiveAborted(reason, source=source)
+        check(rc, "ring_allreduce")
+        return ReduceStats(stats.tx_payload_bytes, stats.rx_payload_bytes)
+
+    def restore(self, buffer: torch.Tensor) -> None:
+        """Hand back the last op's input bytes (completion veto, client.py:973-983)."""
+        check(
+            lib().pcclb_ring_restore(self._handle, buffer.data_ptr(), buffer.numel(), DTYPE_CODE[buffer.dtype],
+                                     torch.cuda.current_stream(self.device).cuda_stream),
+            "ring_restore",
+        )
+
+
+def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
+    """torchrun-style init (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    if not dist.is_initialized():
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend or "gloo", rank=rank, world_size=world)
+    return rank, world, local

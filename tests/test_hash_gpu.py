@@ -1,0 +1,93 @@
+"""simplehash on the GPU vs the reference's known answers and the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import simplehash as osh
+from tests.golden.gen import hash_bytes
+from tests.gpu_util import need_gpu, to_dev
+from tests.test_oracle_golden import _hash_input
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def test_kats_one_by_one(golden):
+    from paper_2505_14065_b200 import simplehash
+
+    for k in golden["hash"]:
+        buf = to_dev(_hash_input(k))
+        assert simplehash(buf) == k["hash"], k["name"]
+
+
+def test_kats_multi_entry_single_launch(golden):
+    from paper_2505_14065_b200 import simplehash_many
+
+    ks = golden["hash"]
+    bufs = [to_dev(_hash_input(k)) for k in ks]
+    assert simplehash_many(bufs) == [k["hash"] for k in ks]
+
+
+@pytest.mark.parametrize("offset", list(range(1, 16)))
+def test_misaligned_views(offset):
+    from paper_2505_14065_b200 import simplehash
+
+    raw = hash_bytes(300_000 + offset)
+    d = to_dev(raw)
+    for start in (offset, offset + 1024):
+        view = d[start:]
+        assert simplehash(view) == osh.simplehash_c(raw[start:])
+
+
+def test_dtype_agnostic_raw_bytes():
+    from paper_2505_14065_b200 import simplehash
+
+    x = torch.randn(12345, dtype=torch.bfloat16, device="cuda")
+    raw = x.view(torch.uint8).cpu().numpy()
+    assert simplehash(x) == osh.simplehash_c(raw)
+
+
+def test_host_buffers_stream_through_device(golden):
+    from paper_2505_14065_b200 import simplehash
+    from paper_2505_14065_b200.sharedstate import StreamingHasher
+
+    k = next(k for k in golden["hash"] if k["name"] == "rng2_64MiB")
+    buf = _hash_input(k)
+    assert simplehash(buf.tobytes()) == k["hash"]
+    small = StreamingHasher(segment_bytes=1 << 20)  # many segments
+    assert small.hash(buf) == k["hash"]
+    assert small.hash(b"") == next(x["hash"] for x in golden["hash"] if x["name"] == "empty")
+
+
+def test_llama_like_layout_scaled():
+    """Many entries of very different sizes in one launch (config-4 shape, scaled)."""
+    from paper_2505_14065_b200 import digest_entries
+    from paper_2505_14065_b200.sharedstate import DType, SharedStateEntry
+
+    rng = np.random.default_rng(9)
+    shapes = [(1283, 64), (1283, 64)] + [(64, 64), (16, 64), (16, 64), (64, 64), (143, 64), (143, 64), (64, 143), (64,), (64,)] * 8
+    entries = []
+    host = []
+    for i, sh in enumerate(shapes):
+        t = torch.from_numpy(rng.normal(0, 1, int(np.prod(sh))).astype(np.float32)).to(torch.bfloat16).cuda()
+        entries.append(SharedStateEntry(f"e{i}", DType.U8, t.view(torch.uint8)))
+        host.append(t.view(torch.uint8).cpu().numpy())
+    got = digest_entries(entries)
+    want = osh.simplehash_many_c(host, threads=4)
+    assert [h for _, _, h in got] == want
+
+
+def test_one_bit_drift_detected():
+    from paper_2505_14065_b200 import simplehash
+
+    x = torch.randint(0, 256, (1 << 22,), dtype=torch.uint8, device="cuda")
+    h0 = simplehash(x)
+    x[123457] ^= 4
+    assert simplehash(x) != h0
