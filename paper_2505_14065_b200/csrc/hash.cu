@@ -5,14 +5,16 @@
 // offset basis; lanes fold by a depth-8 tree (a ^ rotl(b, 27)) * P over pairs
 // (2j, 2j+1); root ^ byte length.
 //
-// Mapping: one 256-thread CTA per entry, thread t = lane t, so a warp reads
-// 128 contiguous bytes per round and every chain stays in one register pair.
-// Entries stream HBM -> shared memory through a 4-stage ring of 16 KiB TMA
-// bulk copies (cp.async.bulk + mbarrier complete_tx), issued by one thread,
-// so the per-word chain reads shared memory instead of waiting on DRAM.
-// A single entry is bounded by the chain latency (LOP3 -> IMAD.WIDE per word
-// and lane); many entries in flight make the launch HBM-bound,
-// hence the multi-entry launch with largest-first static assignment.
+// Mapping: an entry's 256 lanes are split over kGroups = 4 CTAs of 64
+// threads (thread t = lane 64g + t), so one entry keeps 4 SMs' worth of
+// copies in flight and its chains are the only limit (one
+// LOP3 -> IMAD.WIDE step per word and lane, ~200 GB/s per entry at 1.97 GHz).
+// Each CTA streams its 256-byte slice of every 1 KiB round HBM -> shared
+// memory through a 4-stage ring of 16 KiB stages filled by cp.async.bulk
+// (TMA) copies completing on an mbarrier, so the chain reads shared memory
+// instead of waiting on DRAM. Many entries in flight make the launch
+// HBM-bound; entries are dealt largest first so the longest chains start
+// first. The last group of an entry to finish runs the depth-8 tree fold.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,8 +28,11 @@ namespace pcclb {
 
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kHashThreads = 256;
-constexpr int kStageBytes = 16384;  // 16 rounds of 1 KiB
+constexpr int kGroupLanes = 64;                     // lanes (threads) per CTA
+constexpr int kGroups = 256 / kGroupLanes;          // CTAs per entry
+constexpr int kSliceBytes = kGroupLanes * 4;        // a group's slice of one round
+constexpr int kRoundsPerStage = 64;
+constexpr int kStageBytes = kRoundsPerStage * kSliceBytes;  // 16 KiB
 constexpr int kStages = 4;
 constexpr int kHashSmem = kStageBytes * kStages;
 constexpr int kMaxBatch = 1024;
@@ -108,114 +113,139 @@ __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t ava
   return w;
 }
 
-// Run every lane of one segment. Lane t = threadIdx.x; h is that lane's state.
-// Must be called by all 256 threads of the CTA (uses __syncthreads).
-__device__ __forceinline__ uint64_t hash_segment(const uint8_t *p, uint64_t nbytes, uint64_t h,
-                                                 uint8_t *stage, uint64_t *bars,
-                                                 uint32_t &parity) {
+// Run lanes [lane0, lane0 + kGroupLanes) of one segment; thread t owns lane
+// lane0 + t and h is that lane's running state. Full 1 KiB rounds stream
+// through a kStages-deep ring of shared-memory stages, each filled by up to
+// kRoundsPerStage bulk copies of the group's 256-byte slice of a round.
+// Must be called by all threads of the CTA (uses __syncthreads).
+__device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes, uint32_t lane0,
+                                               uint64_t h, uint8_t *stage, uint64_t *bars,
+                                               uint32_t &parity) {
   const int tid = threadIdx.x;
+  const uint32_t lane = lane0 + tid;
   const uint64_t full_words = nbytes >> 2;
   const uint64_t rounds = full_words >> 8;
   if (rounds > 0 && ((uintptr_t)p & 15) == 0) {
-    const uint64_t bulk = rounds << 10;
-    const uint64_t nst = (bulk + kStageBytes - 1) / kStageBytes;
-    if (tid == 0) {
-      for (uint64_t s = 0; s < nst && s < (uint64_t)kStages; ++s) {
-        uint32_t bytes = (uint32_t)min((uint64_t)kStageBytes, bulk - s * kStageBytes);
-        mbar_expect_tx(&bars[s], bytes);
-        bulk_g2s(stage + s * kStageBytes, p + s * kStageBytes, bytes, &bars[s]);
-      }
-    }
+    const uint64_t nst = (rounds + kRoundsPerStage - 1) / kRoundsPerStage;
+    const uint8_t *src0 = p + lane0 * 4;
+    // warp 0 fills stage slot `slot` with rounds [s*R, s*R + rows)
+    auto issue = [&](uint64_t s, int slot) {
+      const uint32_t rows = (uint32_t)min((uint64_t)kRoundsPerStage, rounds - s * kRoundsPerStage);
+      if (tid == 0) mbar_expect_tx(&bars[slot], rows * kSliceBytes);
+      __syncwarp();
+      uint8_t *dst = stage + slot * kStageBytes;
+      const uint8_t *src = src0 + s * kRoundsPerStage * 1024;
+      for (uint32_t i = tid; i < rows; i += 32)
+        bulk_g2s(dst + i * kSliceBytes, src + (uint64_t)i * 1024, kSliceBytes, &bars[slot]);
+    };
+    if (tid < 32)
+      for (uint64_t s = 0; s < nst && s < (uint64_t)kStages; ++s) issue(s, (int)s);
     for (uint64_t st = 0; st < nst; ++st) {
       const int slot = (int)(st % kStages);
       mbar_wait(&bars[slot], (parity >> slot) & 1u);
       parity ^= 1u << slot;
       const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * kStageBytes) + tid;
-      const uint64_t left = bulk - st * kStageBytes;
+      const uint64_t left = rounds - st * kRoundsPerStage;
       Fnv f(h);
-      if (left >= (uint64_t)kStageBytes) {
-#pragma unroll
-        for (int r = 0; r < kStageBytes / 1024; ++r) f.step(wds[r * 256]);
+      if (left >= (uint64_t)kRoundsPerStage) {
+#pragma unroll 16
+        for (int r = 0; r < kRoundsPerStage; ++r) f.step(wds[r * kGroupLanes]);
       } else {
-        const int nr = (int)(left >> 10);
-        for (int r = 0; r < nr; ++r) f.step(wds[r * 256]);
+        const int nr = (int)left;
+        for (int r = 0; r < nr; ++r) f.step(wds[r * kGroupLanes]);
       }
       h = f.value();
       __syncthreads();  // every lane done with this slot before it is refilled
-      if (tid == 0 && st + kStages < nst) {
-        const uint64_t s = st + kStages;
-        uint32_t bytes = (uint32_t)min((uint64_t)kStageBytes, bulk - s * kStageBytes);
-        mbar_expect_tx(&bars[slot], bytes);
-        bulk_g2s(stage + slot * kStageBytes, p + s * kStageBytes, bytes, &bars[slot]);
-      }
+      if (tid < 32 && st + kStages < nst) issue(st + kStages, slot);
     }
   } else {
-    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + tid) * 4, 4));
+    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
   }
   const uint64_t done = rounds << 8;
   const uint64_t rem = full_words - done;  // < 256
   const uint8_t *q = p + done * 4;
-  if ((uint64_t)tid < rem) h = fnv_step(h, load_word_any(q + 4 * tid, 4));
+  if ((uint64_t)lane < rem) h = fnv_step(h, load_word_any(q + 4 * lane, 4));
   const uint32_t tail = (uint32_t)(nbytes & 3);
-  if (tail && (uint64_t)tid == rem) h = fnv_step(h, load_word_any(q + 4 * tid, tail));
+  if (tail && (uint64_t)lane == rem) h = fnv_step(h, load_word_any(q + 4 * lane, tail));
   return h;
 }
 
-// depth-8 tree over lanes in shared memory; returns root (valid in thread 0)
-__device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s, uint64_t h) {
-  const int tid = threadIdx.x;
-  lane_s[tid] = h;
+// depth-8 tree over 256 lanes in shared memory (pairs (2j, 2j+1), lower is a);
+// any CTA size; returns the root in every thread
+__device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   __syncthreads();
   for (int width = 128; width >= 1; width >>= 1) {
-    uint64_t v = 0;
-    if (tid < width) v = (lane_s[2 * tid] ^ rotl27(lane_s[2 * tid + 1])) * kFnvPrime;
+    uint64_t v[4];
+    int k = 0;
+    for (int j = tid; j < width; j += nt) v[k++] = (lane_s[2 * j] ^ rotl27(lane_s[2 * j + 1])) * kFnvPrime;
     __syncthreads();
-    if (tid < width) lane_s[tid] = v;
+    k = 0;
+    for (int j = tid; j < width; j += nt) lane_s[j] = v[k++];
     __syncthreads();
   }
   return lane_s[0];
 }
 
-__global__ void __launch_bounds__(kHashThreads) simplehash_batch_kernel(const __grid_constant__ HashBatch b) {
-  extern __shared__ __align__(1024) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ uint64_t lane_s[kHashThreads];
+__device__ __forceinline__ void init_bars(uint64_t *bars) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
+}
+
+// Work item = (entry, lane group); entries arrive largest first, so the
+// longest chains start first. The last group of an entry to finish folds.
+__global__ void __launch_bounds__(kGroupLanes)
+    simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *arrived) {
+  extern __shared__ __align__(1024) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ uint64_t lane_s[256];
+  __shared__ uint32_t s_last;
+  init_bars(bars);
   uint32_t parity = 0;
-  for (uint32_t e = blockIdx.x; e < b.count; e += gridDim.x) {
+  const uint32_t items = b.count * kGroups;
+  for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const uint32_t e = it / kGroups, g = it % kGroups;
     const HashEntry E = b.e[e];
-    uint64_t h = hash_segment(E.ptr, E.nbytes, kFnvOffset, stage, bars, parity);
-    uint64_t root = tree_fold(lane_s, h);
-    if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+    const uint32_t lane0 = g * kGroupLanes;
+    uint64_t h = hash_group(E.ptr, E.nbytes, lane0, kFnvOffset, stage, bars, parity);
+    lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&arrived[e], 1u) == kGroups - 1) ? 1u : 0u;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int j = threadIdx.x; j < 256; j += blockDim.x)
+        lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
+      uint64_t root = tree_fold(lane_s);
+      if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+    }
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kHashThreads)
+// streaming update: grid = kGroups CTAs, lane state in/out (no fold)
+__global__ void __launch_bounds__(kGroupLanes)
     simplehash_update_kernel(uint64_t *state, const uint8_t *p, uint64_t nbytes) {
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[kStages];
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
+  init_bars(bars);
   uint32_t parity = 0;
-  uint64_t h = state[threadIdx.x];
-  h = hash_segment(p, nbytes, h, stage, bars, parity);
-  state[threadIdx.x] = h;
+  const uint32_t lane = blockIdx.x * kGroupLanes + threadIdx.x;
+  uint64_t h = hash_group(p, nbytes, blockIdx.x * kGroupLanes, state[lane], stage, bars, parity);
+  state[lane] = h;
 }
 
 __global__ void simplehash_init_kernel(uint64_t *state) { state[threadIdx.x] = kFnvOffset; }
 
-__global__ void __launch_bounds__(kHashThreads)
+__global__ void __launch_bounds__(256)
     simplehash_final_kernel(const uint64_t *state, uint64_t total, uint64_t *out) {
-  __shared__ uint64_t lane_s[kHashThreads];
-  uint64_t root = tree_fold(lane_s, state[threadIdx.x]);
+  __shared__ uint64_t lane_s[256];
+  lane_s[threadIdx.x] = state[threadIdx.x];
+  uint64_t root = tree_fold(lane_s);
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
@@ -256,11 +286,19 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
   cudaStream_t s = as_stream(stream);
   int occ = 0;
   PCCLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, simplehash_batch_kernel,
-                                                           kHashThreads, kHashSmem));
+                                                           kGroupLanes, kHashSmem));
   if (occ < 1) occ = 1;
   const uint32_t slots = (uint32_t)(sm_count() * occ);
+  // per-launch scratch: lane values + per-entry arrival counters
+  const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
+  const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
+  void *scratch = nullptr;
+  PCCLB_CUDA(cudaMallocAsync(&scratch, lanes_bytes + (size_t)m_max * sizeof(uint32_t), s));
+  uint64_t *lanes = static_cast<uint64_t *>(scratch);
+  uint32_t *arrived = reinterpret_cast<uint32_t *>(static_cast<char *>(scratch) + lanes_bytes);
   static thread_local HashBatch batch;
-  for (uint32_t base = 0; base < count; base += kMaxBatch) {
+  rc = PCCLB_OK;
+  for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
     uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
     batch.count = m;
     for (uint32_t i = 0; i < m; ++i) {
@@ -269,11 +307,19 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
       batch.e[i].nbytes = h_nbytes[k];
       batch.e[i].out = d_out + k;
     }
-    unsigned grid = std::min<uint32_t>(m, slots);
-    simplehash_batch_kernel<<<grid, kHashThreads, kHashSmem, s>>>(batch);
-    PCCLB_LAUNCH_CHECK();
+    cudaError_t e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
+    if (e != cudaSuccess) {
+      rc = cuda_status(e);
+      break;
+    }
+    unsigned grid = std::min<uint32_t>(m * kGroups, slots);
+    simplehash_batch_kernel<<<grid, kGroupLanes, kHashSmem, s>>>(batch, lanes, arrived);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_status(e);
   }
-  return PCCLB_OK;
+  cudaError_t e = cudaFreeAsync(scratch, s);
+  if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
+  return rc;
 }
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {
@@ -282,7 +328,7 @@ int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void 
 
 int pcclb_simplehash_init(uint64_t *d_state, void *stream) {
   if (!d_state) return PCCLB_EINVAL;
-  simplehash_init_kernel<<<1, kHashThreads, 0, as_stream(stream)>>>(d_state);
+  simplehash_init_kernel<<<1, 256, 0, as_stream(stream)>>>(d_state);
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
 }
@@ -292,7 +338,7 @@ int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uint64_t nbyt
   if (nbytes == 0) return PCCLB_OK;
   int rc = prepare_hash_kernels();
   if (rc) return rc;
-  simplehash_update_kernel<<<1, kHashThreads, kHashSmem, as_stream(stream)>>>(
+  simplehash_update_kernel<<<kGroups, kGroupLanes, kHashSmem, as_stream(stream)>>>(
       d_state, static_cast<const uint8_t *>(d_data), nbytes);
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
@@ -301,7 +347,7 @@ int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uint64_t nbyt
 int pcclb_simplehash_final(const uint64_t *d_state, uint64_t total_nbytes, uint64_t *d_out,
                            void *stream) {
   if (!d_state || !d_out) return PCCLB_EINVAL;
-  simplehash_final_kernel<<<1, kHashThreads, 0, as_stream(stream)>>>(d_state, total_nbytes, d_out);
+  simplehash_final_kernel<<<1, 256, 0, as_stream(stream)>>>(d_state, total_nbytes, d_out);
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
 }

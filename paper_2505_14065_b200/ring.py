@@ -27,7 +27,10 @@ class LocalRing:
         if world < 1 or world > 64:
             raise UsageError("world must be in [1, 64]")
         self.world = world
-        self.device = torch.device(device or "cuda")
+        dev = torch.device(device or "cuda")
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self.backup_enabled = backup
         nbytes = int(lib().pcclb_local_scratch_bytes(world))
         self.scratch = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=self.device)

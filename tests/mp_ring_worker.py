@@ -1,0 +1,167 @@
+"""Per-rank body of the multi-GPU ring tests (one process per GPU).
+
+Run as ``python tests/mp_ring_worker.py <world> <port> <outdir> [scenario...]``
+by tests/test_ring_ipc_gpu.py through torch.multiprocessing; results are
+written to ``<outdir>/rank<r>.json`` and asserted by the parent.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def _hash(t) -> int:
+    from oracle import simplehash as osh
+
+    return osh.simplehash_c(t.cpu().numpy())
+
+
+def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> None:
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ring as oring
+    from paper_2505_14065_b200.collective import CollectiveAborted
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
+    from paper_2505_14065_b200.schedule import payload_bytes
+    from tests.golden.gen import RING_CASES, ring_inputs
+
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        golden = json.load(f)
+    dev = torch.device("cuda", rank)
+    out: dict = {"rank": rank, "checks": [], "errors": []}
+
+    def check(name, ok, detail=""):
+        out["checks"].append({"name": name, "ok": bool(ok), "detail": str(detail)[:300]})
+
+    try:
+        ring = DeviceRing(device=dev, capacity_bytes=64 << 20, timeout_s=20.0)
+        rev = None
+        if "golden" in scenarios:
+            # every golden case with W == world, in identity and reversed ring order
+            rev = DeviceRing(device=dev, ring=list(reversed(range(world))), capacity_bytes=64 << 20, timeout_s=20.0)
+            for idx, case in enumerate(RING_CASES):
+                w, n, op, quant, dt, seed = case
+                if w != world:
+                    continue
+                want = golden["ring"][idx]["output_hash"]
+                inputs = ring_inputs(w, n, np.dtype(dt), seed)
+                for eng, tag in ((ring, "id"), (rev, "rev")):
+                    pos = eng.position
+                    buf = torch.from_numpy(inputs[pos].copy()).to(dev)
+                    st = eng.run_all_reduce(buf, op, quantize=quant)
+                    check(f"golden[{idx}]/{tag} w={w} n={n} {op} q={quant} {dt}", _hash(buf) == want)
+                    esz = 1 if quant else np.dtype(dt).itemsize
+                    exp = payload_bytes(n, w, esz, pos)
+                    check(f"traffic[{idx}]/{tag}", st.tx_payload_bytes == exp and st.rx_payload_bytes == exp,
+                          f"{st.tx_payload_bytes} vs {exp}")
+        if "faults" in scenarios:
+            n = 40_003
+            for quant in (False, True):
+                nb = world if quant else 2
+                for k in range(nb):
+                    f = k % world
+                    inputs = ring_inputs(world, n, np.dtype("float32"), 500 + k)
+                    mine = inputs[ring.position]
+                    buf = torch.from_numpy(mine.copy()).to(dev)
+                    aborted = False
+                    try:
+                        ring.run_all_reduce(buf, "sum", quantize=quant, fault_at=k if rank == f else -1)
+                    except CollectiveAborted:
+                        aborted = True
+                    check(f"fault q={quant} at={k} by={f}: aborted", aborted)
+                    check(f"fault q={quant} at={k}: restored", buf.cpu().numpy().tobytes() == mine.tobytes())
+                    # survivors retry the same op: bit-exact
+                    ring.run_all_reduce(buf, "sum", quantize=quant)
+                    want = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.SUM, quantize=quant)
+                    check(f"fault q={quant} at={k}: retry exact", buf.cpu().numpy().tobytes() == want.tobytes())
+            # host abort word (the control plane's ABORT_NOTIFY)
+            inputs = ring_inputs(world, n, np.dtype("float32"), 900)
+            mine = inputs[ring.position]
+            buf = torch.from_numpy(mine.copy()).to(dev)
+            if rank == world - 1:
+                ring.signal_abort()
+            aborted = False
+            try:
+                ring.run_all_reduce(buf, "avg")
+            except CollectiveAborted as e:
+                aborted = e.source in ("master", "io")
+            ring.reset_abort()
+            check("host abort: aborted", aborted)
+            check("host abort: restored", buf.cpu().numpy().tobytes() == mine.tobytes())
+            dist.barrier()
+            ring.run_all_reduce(buf, "avg")
+            want = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.AVG)
+            check("host abort: retry exact", buf.cpu().numpy().tobytes() == want.tobytes())
+            # non-finite under quantization: everyone aborts and restores
+            inputs = ring_inputs(world, n, np.dtype("float32"), 901)
+            inputs[world // 2][77] = np.inf
+            mine = inputs[ring.position]
+            buf = torch.from_numpy(mine.copy()).to(dev)
+            aborted = False
+            try:
+                ring.run_all_reduce(buf, "sum", quantize=True)
+            except CollectiveAborted:
+                aborted = True
+            check("nonfinite: aborted", aborted)
+            check("nonfinite: restored", buf.cpu().numpy().tobytes() == mine.tobytes())
+            # completion veto restore (client.py:973-983)
+            inputs = ring_inputs(world, n, np.dtype("float64"), 902)
+            mine = inputs[ring.position]
+            buf = torch.from_numpy(mine.copy()).to(dev)
+            ring.run_all_reduce(buf, "max")
+            ring.restore(buf)
+            check("veto restore", buf.cpu().numpy().tobytes() == mine.tobytes())
+        if "large" in scenarios:
+            n = (1 << 24) + 3
+            for quant in (False, True):
+                inputs = [np.random.default_rng(70 + p).normal(0, 1, n).astype(np.float32) for p in range(world)]
+                buf = torch.from_numpy(inputs[ring.position].copy()).to(dev)
+                ring.run_all_reduce(buf, "avg", quantize=quant)
+                got = buf.cpu().numpy()
+                # each rank verifies its owned chunk and one other chunk against the oracle
+                bounds = oring.chunk_bounds(n, world)
+                for c in {(ring.position + 1) % world, ring.position}:
+                    lo, hi = bounds[c]
+                    spans = [inputs[(c + k) % world][lo:hi] for k in range(world)]
+                    want = oring.reduce_chunk(spans, oring.ReduceOp.AVG, quant, world)
+                    check(f"large q={quant} chunk {c}", got[lo:hi].tobytes() == want.tobytes())
+                hs = [None] * world
+                dist.all_gather_object(hs, _hash(buf))
+                check(f"large q={quant}: identical on all ranks", len(set(hs)) == 1)
+        ring.close()
+        if rev is not None:
+            rev.close()
+    except Exception:  # noqa: BLE001
+        out["errors"].append(traceback.format_exc())
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+        json.dump(out, f)
+    try:
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        pass
+
+
+def _entry(rank, world, port, outdir, scenarios):
+    run(rank, world, port, outdir, scenarios)
+
+
+if __name__ == "__main__":
+    import torch.multiprocessing as mp
+
+    world, port, outdir = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    scenarios = sys.argv[4:] or ["golden", "faults", "large"]
+    mp.spawn(_entry, args=(world, port, outdir, scenarios), nprocs=world, join=True)

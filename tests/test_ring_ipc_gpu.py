@@ -1,0 +1,51 @@
+"""Multi-GPU (one process per GPU) ring all-reduce over NVLink: bit-exact vs
+the reference goldens in identity and reversed ring order, traffic identity,
+abort atomicity at every synchronisation point (mirroring
+test_ring_engine.py:136-174 and test_acceptance.py:127-154), host abort,
+non-finite abort, veto restore, and config-sized chunks vs the oracle."""
+
+from __future__ import annotations
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worlds():
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    ws = [w for w in (2, 3, 4, 8) if w <= n]
+    return ws or [2]
+
+
+@pytest.mark.parametrize("world", _worlds())
+def test_nvlink_ring(world, tmp_path):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, os.path.join(ROOT, "tests", "mp_ring_worker.py"), str(world), str(_free_port()), str(tmp_path)]
+    proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0, proc.stderr[-4000:]
+    failures = []
+    total = 0
+    for r in range(world):
+        with open(tmp_path / f"rank{r}.json") as f:
+            res = json.load(f)
+        assert not res["errors"], res["errors"][0]
+        total += len(res["checks"])
+        failures += [(r, c["name"], c["detail"]) for c in res["checks"] if not c["ok"]]
+    assert total > 0
+    assert not failures, failures[:20]
