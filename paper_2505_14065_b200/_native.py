@@ -57,7 +57,12 @@ class QMeta(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("tx_payload_bytes", ctypes.c_uint64), ("rx_payload_bytes", ctypes.c_uint64)]
+    _fields_ = [
+        ("tx_payload_bytes", ctypes.c_uint64),
+        ("rx_payload_bytes", ctypes.c_uint64),
+        ("n_phases", ctypes.c_uint32),
+        ("phase_ms", ctypes.c_float * 15),
+    ]
 
 
 _P = ctypes.c_void_p

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <numeric>
 #include <vector>
@@ -28,13 +29,6 @@ namespace pcclb {
 
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kGroupLanes = 64;                     // lanes (threads) per CTA
-constexpr int kGroups = 256 / kGroupLanes;          // CTAs per entry
-constexpr int kSliceBytes = kGroupLanes * 4;        // a group's slice of one round
-constexpr int kRoundsPerStage = 64;
-constexpr int kStageBytes = kRoundsPerStage * kSliceBytes;  // 16 KiB
-constexpr int kStages = 4;
-constexpr int kHashSmem = kStageBytes * kStages;
 constexpr int kMaxBatch = 1024;
 
 struct HashEntry {
@@ -113,11 +107,24 @@ __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t ava
   return w;
 }
 
-// Run lanes [lane0, lane0 + kGroupLanes) of one segment; thread t owns lane
-// lane0 + t and h is that lane's running state. Full 1 KiB rounds stream
-// through a kStages-deep ring of shared-memory stages, each filled by up to
-// kRoundsPerStage bulk copies of the group's 256-byte slice of a round.
+// Kernel shape: LANES threads per CTA (thread t = lane lane0 + t), a ring of
+// STAGES shared-memory stages of ROWS rounds each. A stage holds the CTA's
+// LANES*4-byte slice of ROWS consecutive 1 KiB rounds; with LANES == 256 the
+// slices are contiguous and a stage is ONE bulk copy.
+template <int LANES_, int ROWS_, int STAGES_>
+struct HashCfg {
+  static constexpr int LANES = LANES_;
+  static constexpr int ROWS = ROWS_;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int GROUPS = 256 / LANES;
+  static constexpr int SLICE = LANES * 4;
+  static constexpr int STAGE_BYTES = ROWS * SLICE;
+  static constexpr int SMEM = STAGE_BYTES * STAGES;
+};
+
+// Run lanes [lane0, lane0 + LANES) of one segment; h is the lane's state.
 // Must be called by all threads of the CTA (uses __syncthreads).
+template <class C>
 __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes, uint32_t lane0,
                                                uint64_t h, uint8_t *stage, uint64_t *bars,
                                                uint32_t &parity) {
@@ -126,37 +133,44 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
   const uint64_t full_words = nbytes >> 2;
   const uint64_t rounds = full_words >> 8;
   if (rounds > 0 && ((uintptr_t)p & 15) == 0) {
-    const uint64_t nst = (rounds + kRoundsPerStage - 1) / kRoundsPerStage;
+    const uint64_t nst = (rounds + C::ROWS - 1) / C::ROWS;
     const uint8_t *src0 = p + lane0 * 4;
-    // warp 0 fills stage slot `slot` with rounds [s*R, s*R + rows)
+    // warp 0 fills stage slot `slot` with rounds [s*ROWS, s*ROWS + rows)
     auto issue = [&](uint64_t s, int slot) {
-      const uint32_t rows = (uint32_t)min((uint64_t)kRoundsPerStage, rounds - s * kRoundsPerStage);
-      if (tid == 0) mbar_expect_tx(&bars[slot], rows * kSliceBytes);
-      __syncwarp();
-      uint8_t *dst = stage + slot * kStageBytes;
-      const uint8_t *src = src0 + s * kRoundsPerStage * 1024;
-      for (uint32_t i = tid; i < rows; i += 32)
-        bulk_g2s(dst + i * kSliceBytes, src + (uint64_t)i * 1024, kSliceBytes, &bars[slot]);
+      const uint32_t rows = (uint32_t)min((uint64_t)C::ROWS, rounds - s * C::ROWS);
+      uint8_t *dst = stage + slot * C::STAGE_BYTES;
+      const uint8_t *src = src0 + s * C::ROWS * 1024;
+      if constexpr (C::LANES == 256) {
+        if (tid == 0) {
+          mbar_expect_tx(&bars[slot], rows * 1024);
+          bulk_g2s(dst, src, rows * 1024, &bars[slot]);
+        }
+      } else {
+        if (tid == 0) mbar_expect_tx(&bars[slot], rows * C::SLICE);
+        __syncwarp();
+        for (uint32_t i = tid; i < rows; i += 32)
+          bulk_g2s(dst + i * C::SLICE, src + (uint64_t)i * 1024, C::SLICE, &bars[slot]);
+      }
     };
     if (tid < 32)
-      for (uint64_t s = 0; s < nst && s < (uint64_t)kStages; ++s) issue(s, (int)s);
+      for (uint64_t s = 0; s < nst && s < (uint64_t)C::STAGES; ++s) issue(s, (int)s);
     for (uint64_t st = 0; st < nst; ++st) {
-      const int slot = (int)(st % kStages);
+      const int slot = (int)(st % C::STAGES);
       mbar_wait(&bars[slot], (parity >> slot) & 1u);
       parity ^= 1u << slot;
-      const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * kStageBytes) + tid;
-      const uint64_t left = rounds - st * kRoundsPerStage;
+      const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
+      const uint64_t left = rounds - st * C::ROWS;
       Fnv f(h);
-      if (left >= (uint64_t)kRoundsPerStage) {
+      if (left >= (uint64_t)C::ROWS) {
 #pragma unroll 16
-        for (int r = 0; r < kRoundsPerStage; ++r) f.step(wds[r * kGroupLanes]);
+        for (int r = 0; r < C::ROWS; ++r) f.step(wds[r * C::LANES]);
       } else {
         const int nr = (int)left;
-        for (int r = 0; r < nr; ++r) f.step(wds[r * kGroupLanes]);
+        for (int r = 0; r < nr; ++r) f.step(wds[r * C::LANES]);
       }
       h = f.value();
       __syncthreads();  // every lane done with this slot before it is refilled
-      if (tid < 32 && st + kStages < nst) issue(st + kStages, slot);
+      if (tid < 32 && st + C::STAGES < nst) issue(st + C::STAGES, slot);
     }
   } else {
     for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
@@ -176,20 +190,21 @@ __device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s) {
   const int tid = threadIdx.x, nt = blockDim.x;
   __syncthreads();
   for (int width = 128; width >= 1; width >>= 1) {
-    uint64_t v[4];
-    int k = 0;
-    for (int j = tid; j < width; j += nt) v[k++] = (lane_s[2 * j] ^ rotl27(lane_s[2 * j + 1])) * kFnvPrime;
+    uint64_t v0 = 0, v1 = 0;  // nt >= 64 => at most 2 pairs per thread
+    if (tid < width) v0 = (lane_s[2 * tid] ^ rotl27(lane_s[2 * tid + 1])) * kFnvPrime;
+    if (tid + nt < width) v1 = (lane_s[2 * (tid + nt)] ^ rotl27(lane_s[2 * (tid + nt) + 1])) * kFnvPrime;
     __syncthreads();
-    k = 0;
-    for (int j = tid; j < width; j += nt) lane_s[j] = v[k++];
+    if (tid < width) lane_s[tid] = v0;
+    if (tid + nt < width) lane_s[tid + nt] = v1;
     __syncthreads();
   }
   return lane_s[0];
 }
 
+template <int STAGES>
 __device__ __forceinline__ void init_bars(uint64_t *bars) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -197,45 +212,53 @@ __device__ __forceinline__ void init_bars(uint64_t *bars) {
 
 // Work item = (entry, lane group); entries arrive largest first, so the
 // longest chains start first. The last group of an entry to finish folds.
-__global__ void __launch_bounds__(kGroupLanes)
+template <class C>
+__global__ void __launch_bounds__(C::LANES)
     simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *arrived) {
   extern __shared__ __align__(1024) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ __align__(8) uint64_t bars[C::STAGES];
   __shared__ uint64_t lane_s[256];
   __shared__ uint32_t s_last;
-  init_bars(bars);
+  init_bars<C::STAGES>(bars);
   uint32_t parity = 0;
-  const uint32_t items = b.count * kGroups;
+  const uint32_t items = b.count * C::GROUPS;
   for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const uint32_t e = it / kGroups, g = it % kGroups;
+    const uint32_t e = it / C::GROUPS, g = it % C::GROUPS;
     const HashEntry E = b.e[e];
-    const uint32_t lane0 = g * kGroupLanes;
-    uint64_t h = hash_group(E.ptr, E.nbytes, lane0, kFnvOffset, stage, bars, parity);
-    lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&arrived[e], 1u) == kGroups - 1) ? 1u : 0u;
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      for (int j = threadIdx.x; j < 256; j += blockDim.x)
-        lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
+    const uint32_t lane0 = g * C::LANES;
+    uint64_t h = hash_group<C>(E.ptr, E.nbytes, lane0, kFnvOffset, stage, bars, parity);
+    if constexpr (C::GROUPS == 1) {
+      lane_s[threadIdx.x] = h;
       uint64_t root = tree_fold(lane_s);
       if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+    } else {
+      lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = (atomicAdd(&arrived[e], 1u) == C::GROUPS - 1) ? 1u : 0u;
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        for (int j = threadIdx.x; j < 256; j += blockDim.x)
+          lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
+        uint64_t root = tree_fold(lane_s);
+        if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+      }
     }
     __syncthreads();
   }
 }
 
-// streaming update: grid = kGroups CTAs, lane state in/out (no fold)
-__global__ void __launch_bounds__(kGroupLanes)
+// streaming update: grid = GROUPS CTAs, lane state in/out (no fold)
+template <class C>
+__global__ void __launch_bounds__(C::LANES)
     simplehash_update_kernel(uint64_t *state, const uint8_t *p, uint64_t nbytes) {
   extern __shared__ __align__(1024) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  init_bars(bars);
+  __shared__ __align__(8) uint64_t bars[C::STAGES];
+  init_bars<C::STAGES>(bars);
   uint32_t parity = 0;
-  const uint32_t lane = blockIdx.x * kGroupLanes + threadIdx.x;
-  uint64_t h = hash_group(p, nbytes, blockIdx.x * kGroupLanes, state[lane], stage, bars, parity);
+  const uint32_t lane = blockIdx.x * C::LANES + threadIdx.x;
+  uint64_t h = hash_group<C>(p, nbytes, blockIdx.x * C::LANES, state[lane], stage, bars, parity);
   state[lane] = h;
 }
 
@@ -249,6 +272,31 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
+// Variants (PCCLB_HASH_VARIANT selects one for experiments; 0 is the default)
+using HashV0 = HashCfg<256, 16, 12>;  // 192 KiB ring, 1 CTA/SM, 16 KiB copies
+using HashV1 = HashCfg<256, 16, 6>;   // 96 KiB ring, 2 CTAs/SM
+using HashV2 = HashCfg<128, 32, 6>;   // 2 CTAs per entry, 512 B slices
+using HashV3 = HashCfg<64, 64, 4>;    // 4 CTAs per entry, 256 B slices
+using HashV4 = HashCfg<128, 32, 12>;  // 2 CTAs per entry, 192 KiB ring
+
+int hash_variant() {
+  static int v = [] {
+    const char *e = getenv("PCCLB_HASH_VARIANT");
+    int x = e ? atoi(e) : 0;
+    return (x < 0 || x > 4) ? 0 : x;
+  }();
+  return v;
+}
+
+template <class C>
+static int prepare_variant() {
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_batch_kernel<C>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_update_kernel<C>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  return PCCLB_OK;
+}
+
 static int prepare_hash_kernels() {
   static std::mutex mu;
   static bool done[64] = {false};
@@ -256,11 +304,69 @@ static int prepare_hash_kernels() {
   PCCLB_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
   if (dev >= 0 && dev < 64 && done[dev]) return PCCLB_OK;
-  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_batch_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem));
-  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_update_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kHashSmem));
+  int rc = prepare_variant<HashV0>();
+  if (!rc) rc = prepare_variant<HashV1>();
+  if (!rc) rc = prepare_variant<HashV2>();
+  if (!rc) rc = prepare_variant<HashV3>();
+  if (!rc) rc = prepare_variant<HashV4>();
+  if (rc) return rc;
   if (dev >= 0 && dev < 64) done[dev] = true;
+  return PCCLB_OK;
+}
+
+template <class C>
+static int launch_batches(const std::vector<uint32_t> &order, const void *const *h_ptrs,
+                          const uint64_t *h_nbytes, uint32_t count, uint64_t *d_out,
+                          cudaStream_t s) {
+  int occ = 0;
+  PCCLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, simplehash_batch_kernel<C>,
+                                                           C::LANES, C::SMEM));
+  if (occ < 1) occ = 1;
+  const uint32_t slots = (uint32_t)(sm_count() * occ);
+  // per-launch scratch: lane values + per-entry arrival counters
+  const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
+  const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
+  void *scratch = nullptr;
+  if (C::GROUPS > 1)
+    PCCLB_CUDA(cudaMallocAsync(&scratch, lanes_bytes + (size_t)m_max * sizeof(uint32_t), s));
+  uint64_t *lanes = static_cast<uint64_t *>(scratch);
+  uint32_t *arrived =
+      scratch ? reinterpret_cast<uint32_t *>(static_cast<char *>(scratch) + lanes_bytes) : nullptr;
+  static thread_local HashBatch batch;
+  int rc = PCCLB_OK;
+  for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
+    uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
+    batch.count = m;
+    for (uint32_t i = 0; i < m; ++i) {
+      uint32_t k = order[base + i];
+      batch.e[i].ptr = static_cast<const uint8_t *>(h_ptrs[k]);
+      batch.e[i].nbytes = h_nbytes[k];
+      batch.e[i].out = d_out + k;
+    }
+    if (arrived) {
+      cudaError_t e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
+      if (e != cudaSuccess) {
+        rc = cuda_status(e);
+        break;
+      }
+    }
+    unsigned grid = std::min<uint32_t>(m * C::GROUPS, slots);
+    simplehash_batch_kernel<C><<<grid, C::LANES, C::SMEM, s>>>(batch, lanes, arrived);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_status(e);
+  }
+  if (scratch) {
+    cudaError_t e = cudaFreeAsync(scratch, s);
+    if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
+  }
+  return rc;
+}
+
+template <class C>
+static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaStream_t s) {
+  simplehash_update_kernel<C><<<C::GROUPS, C::LANES, C::SMEM, s>>>(
+      state, static_cast<const uint8_t *>(d), nbytes);
+  PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
 }
 
@@ -284,42 +390,18 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
   cudaStream_t s = as_stream(stream);
-  int occ = 0;
-  PCCLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, simplehash_batch_kernel,
-                                                           kGroupLanes, kHashSmem));
-  if (occ < 1) occ = 1;
-  const uint32_t slots = (uint32_t)(sm_count() * occ);
-  // per-launch scratch: lane values + per-entry arrival counters
-  const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
-  const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  void *scratch = nullptr;
-  PCCLB_CUDA(cudaMallocAsync(&scratch, lanes_bytes + (size_t)m_max * sizeof(uint32_t), s));
-  uint64_t *lanes = static_cast<uint64_t *>(scratch);
-  uint32_t *arrived = reinterpret_cast<uint32_t *>(static_cast<char *>(scratch) + lanes_bytes);
-  static thread_local HashBatch batch;
-  rc = PCCLB_OK;
-  for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
-    uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
-    batch.count = m;
-    for (uint32_t i = 0; i < m; ++i) {
-      uint32_t k = order[base + i];
-      batch.e[i].ptr = static_cast<const uint8_t *>(h_ptrs[k]);
-      batch.e[i].nbytes = h_nbytes[k];
-      batch.e[i].out = d_out + k;
-    }
-    cudaError_t e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
-    if (e != cudaSuccess) {
-      rc = cuda_status(e);
-      break;
-    }
-    unsigned grid = std::min<uint32_t>(m * kGroups, slots);
-    simplehash_batch_kernel<<<grid, kGroupLanes, kHashSmem, s>>>(batch, lanes, arrived);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) rc = cuda_status(e);
+  switch (hash_variant()) {
+    case 1:
+      return launch_batches<HashV1>(order, h_ptrs, h_nbytes, count, d_out, s);
+    case 2:
+      return launch_batches<HashV2>(order, h_ptrs, h_nbytes, count, d_out, s);
+    case 3:
+      return launch_batches<HashV3>(order, h_ptrs, h_nbytes, count, d_out, s);
+    case 4:
+      return launch_batches<HashV4>(order, h_ptrs, h_nbytes, count, d_out, s);
+    default:
+      return launch_batches<HashV0>(order, h_ptrs, h_nbytes, count, d_out, s);
   }
-  cudaError_t e = cudaFreeAsync(scratch, s);
-  if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
-  return rc;
 }
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {
@@ -338,10 +420,8 @@ int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uint64_t nbyt
   if (nbytes == 0) return PCCLB_OK;
   int rc = prepare_hash_kernels();
   if (rc) return rc;
-  simplehash_update_kernel<<<kGroups, kGroupLanes, kHashSmem, as_stream(stream)>>>(
-      d_state, static_cast<const uint8_t *>(d_data), nbytes);
-  PCCLB_LAUNCH_CHECK();
-  return PCCLB_OK;
+  // a single chain set: the multi-CTA shape keeps more copies in flight
+  return launch_update<HashV4>(d_state, d_data, nbytes, as_stream(stream));
 }
 
 int pcclb_simplehash_final(const uint64_t *d_state, uint64_t total_nbytes, uint64_t *d_out,

@@ -332,7 +332,17 @@ __global__ void __launch_bounds__(kIpcThreads)
 
 using namespace pcclb;
 
+struct PhaseTimer {
+  bool on = false;
+  int n = 0;
+  cudaEvent_t ev[16];
+  void mark(cudaStream_t s) {
+    if (on && n < 16) cudaEventRecord(ev[n++], s);
+  }
+};
+
 struct pcclb_ring {
+  PhaseTimer timer;
   int device;
   uint32_t rank, world;
   uint64_t capacity;
@@ -415,9 +425,12 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
   Signal *me = sig_of(r->ws);
   // copy-in: the caller's bytes become the backup and the peers' fold input
+  r->timer.mark(s);
   PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  r->timer.mark(s);
   int rc = launch_barrier(r, attempt, 0, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
+  r->timer.mark(s);
   if (own_n) {
     FoldArgs<T> f{};
     for (uint32_t k = 0; k < w; ++k)
@@ -450,8 +463,10 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
 #undef PCCLB_IPC_FOLD
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
   rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
+  r->timer.mark(s);
   GatherArgs g{};
   g.mine = me;
   uint32_t jobs = 0;
@@ -474,6 +489,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     ipc_gather_plain_kernel<T><<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
   return PCCLB_OK;
 }
 
@@ -486,6 +502,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   Signal *me = sig_of(r->ws);
   const uint32_t pred = (rank + w - 1) % w;
   Signal *pred_sig = sig_of(r->peer_ws[pred]);
+  r->timer.mark(s);
   PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
   // range slots reset
   PCCLB_CUDA(cudaMemsetAsync(me->range, 0, sizeof(pcclb_range) * (w + 1), s));
@@ -499,6 +516,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     ipc_range_kernel<<<ipc_grid(n0 / 4 + 1), kIpcThreads, 0, s>>>(buf + a0, n0, &me->range[0], me);
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
   int rc;
   for (uint32_t step = 0; step + 1 < w; ++step) {
     const uint32_t tx = (rank + w - step % w) % w;         // (rank - step) mod w
@@ -532,6 +550,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
       PCCLB_LAUNCH_CHECK();
     }
   }
+  r->timer.mark(s);
   // gather prologue: owner adopts D(Q(own)) (collective.py:538-551), fused with AVG
   const uint32_t own = (rank + 1) % w;
   uint64_t oa, on;
@@ -543,6 +562,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   PCCLB_LAUNCH_CHECK();
   rc = launch_barrier(r, attempt, w - 1, fault_at, &me->range[w - 1], timeout_ns, s);
   if (rc) return rc;
+  r->timer.mark(s);
   GatherArgs g{};
   g.mine = me;
   g.avg = avg;
@@ -568,6 +588,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     ipc_gather_quant_kernel<<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
   return PCCLB_OK;
 }
 
@@ -581,8 +602,8 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
   *out = nullptr;
   PCCLB_CUDA(cudaSetDevice(device));
   pcclb_ring *r = new (std::nothrow) pcclb_ring();
+  // value-initialised: pointers null, flags false
   if (!r) return PCCLB_ENOMEM;
-  std::memset(r, 0, sizeof(*r));
   r->device = device;
   r->rank = rank;
   r->world = world;
@@ -602,6 +623,11 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
     return cuda_status(e);
   }
   std::memset((void *)r->host, 0, sizeof(HostFlags));
+  const char *prof = getenv("PCCLB_RING_PROFILE");
+  if (prof && prof[0] == '1') {
+    r->timer.on = true;
+    for (int i = 0; i < 16; ++i) cudaEventCreate(&r->timer.ev[i]);
+  }
   r->peer_ws[rank] = r->ws;
   r->imported[rank] = true;
   *out = r;
@@ -691,6 +717,7 @@ int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int 
     return PCCLB_OK;
   }
   Signal *me = sig_of(r->ws);
+  r->timer.n = 0;
   PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
   const uint64_t timeout_ns = (uint64_t)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
   int rc;
@@ -704,6 +731,14 @@ int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int 
   r->have_backup = true;
   PCCLB_CUDA(cudaMemcpyAsync(r->status_host, &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   PCCLB_CUDA(cudaStreamSynchronize(s));
+  if (out_stats) {
+    out_stats->n_phases = 0;
+    for (int i = 1; i < r->timer.n && i < 16; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, r->timer.ev[i - 1], r->timer.ev[i]);
+      out_stats->phase_ms[out_stats->n_phases++] = ms;
+    }
+  }
   const uint32_t st = *r->status_host;
   if (st == 0) return PCCLB_OK;
   // restore the caller's bytes (collective.py:568-574)
@@ -730,6 +765,8 @@ void pcclb_ring_destroy(pcclb_ring *r) {
   if (r->ws) cudaFree(r->ws);
   if (r->host) cudaFreeHost((void *)r->host);
   if (r->status_host) cudaFreeHost(r->status_host);
+  if (r->timer.on)
+    for (int i = 0; i < 16; ++i) cudaEventDestroy(r->timer.ev[i]);
   delete r;
 }
 

@@ -36,6 +36,7 @@ _STATUS_REASON = {
 class ReduceStats:
     tx_payload_bytes: int
     rx_payload_bytes: int
+    phase_ms: tuple = ()  # filled when PCCLB_RING_PROFILE=1 (csrc/ring_ipc.cu PhaseTimer)
 
 
 def exchange_bytes(payload: bytes, group=None) -> list[bytes]:
@@ -147,7 +148,8 @@ class DeviceRing:
             reason, source = _STATUS_REASON[rc]
             raise CollectiveAborted(reason, source=source)
         check(rc, "ring_allreduce")
-        return ReduceStats(stats.tx_payload_bytes, stats.rx_payload_bytes)
+        phases = tuple(round(stats.phase_ms[i], 4) for i in range(stats.n_phases))
+        return ReduceStats(stats.tx_payload_bytes, stats.rx_payload_bytes, phases)
 
     def restore(self, buffer: torch.Tensor) -> None:
         """Hand back the last op's input bytes (completion veto, client.py:973-983)."""

@@ -1,0 +1,48 @@
+"""Microbenchmark of the simplehash kernel variants (PCCLB_HASH_VARIANT).
+
+Run one variant per process:  PCCLB_HASH_VARIANT=k python tools/hash_variants.py
+Prints one JSON line: config-4 layout, a single 1.05 GB entry, and 64 equal
+64 MiB entries (HBM-bound case), each as ms and GB/s (CUDA events)."""
+
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import llama3_8b_layout  # noqa: E402
+from paper_2505_14065_b200.sharedstate import simplehash_many_async  # noqa: E402
+
+
+def timeit(views, reps=5):
+    out = torch.empty(len(views), dtype=torch.int64, device="cuda")
+    simplehash_many_async(views, out)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        simplehash_many_async(views, out)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    nb = sum(v.numel() * v.element_size() for v in views)
+    return {"ms": round(ms, 3), "GBps": round(nb / ms / 1e6, 1)}, out.cpu().tolist()
+
+
+layout = llama3_8b_layout()
+total = sum(n for _, n in layout)
+state = torch.empty(total, dtype=torch.bfloat16, device="cuda")
+state.view(torch.int16).random_(-32768, 32767)
+views, off = [], 0
+for _, n in layout:
+    views.append(state[off : off + n])
+    off += n
+res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0"))}
+res["config4"], digests = timeit(views)
+res["single_1GB"], _ = timeit([views[0]], 3)
+eq = state[: 64 * (32 << 20)].view(64, -1)
+res["64x64MiB"], _ = timeit([eq[i] for i in range(64)])
+res["digest0"] = digests[0] & 0xFFFFFFFFFFFFFFFF
+print(json.dumps(res))
