@@ -5,20 +5,28 @@
 // offset basis; lanes fold by a depth-8 tree (a ^ rotl(b, 27)) * P over pairs
 // (2j, 2j+1); root ^ byte length.
 //
-// Mapping: an entry's 256 lanes are split over kGroups = 4 CTAs of 64
-// threads (thread t = lane 64g + t), so one entry keeps 4 SMs' worth of
-// copies in flight and its chains are the only limit (one
-// LOP3 -> IMAD.WIDE step per word and lane, ~200 GB/s per entry at 1.97 GHz).
-// Each CTA streams its 256-byte slice of every 1 KiB round HBM -> shared
-// memory through a 4-stage ring of 16 KiB stages filled by cp.async.bulk
-// (TMA) copies completing on an mbarrier, so the chain reads shared memory
-// instead of waiting on DRAM. Many entries in flight make the launch
-// HBM-bound; entries are dealt largest first so the longest chains start
-// first. The last group of an entry to finish runs the depth-8 tree fold.
+// Bounds (measured, tools/micro/chain_micro.cu): one FNV step is a dependent
+// LOP3 -> IMAD.WIDE pair of ~14.3 cycles, so one entry (256 chains) cannot go
+// faster than 1 KiB per 14.3 cycles (~141 GB/s at 1.97 GHz) however many SMs
+// it gets; an SM issues at most ~1 KiB of steps per ~13.4 cycles (~150 GB/s),
+// so the whole chip (~22 TB/s) is far above HBM. Many entries in flight are
+// therefore HBM-bound, and the largest entry sets a latency floor.
+//
+// Mapping (default): an entry's 256 lanes are split over kGroups = 2 CTAs of
+// 128 threads (thread t = lane 128g + t), each on its own SM, so a lone large
+// entry runs at its chain bound. A CTA streams its 512-byte slice of every
+// 1 KiB round through a 6-stage shared-memory ring; each stage (32 rounds) is
+// ONE 2-D TMA copy (cp.async.bulk.tensor.2d, the entry viewed as a
+// [rounds x 256] u32 tensor, box 128 x 32) completing on an mbarrier.
+// Entries are dealt largest first, so the longest chains start first; the
+// last group of an entry to finish runs the tree fold.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <numeric>
 #include <vector>
@@ -29,12 +37,13 @@ namespace pcclb {
 
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kMaxBatch = 1024;
+constexpr int kMaxBatch = 1000;  // HashBatch must fit the 32 KiB kernel-parameter space
 
 struct HashEntry {
   const uint8_t *ptr;
   uint64_t nbytes;
   uint64_t *out;
+  const CUtensorMap *map;  // 2-D view [rounds x 256] u32, or null (fallback loads)
 };
 
 struct HashBatch {
@@ -74,6 +83,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *map, int x, int y,
+                                           uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensormap_acquire(const CUtensorMap *map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(map) : "memory");
+}
 
 // One FNV-1a-64 step h = (h ^ w) * P on the split state (lo, hi).
 // P = 2^40 + 435 and w is a zero-extended u32, so with x = lo ^ w:
@@ -108,52 +128,52 @@ __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t ava
 }
 
 // Kernel shape: LANES threads per CTA (thread t = lane lane0 + t), a ring of
-// STAGES shared-memory stages of ROWS rounds each. A stage holds the CTA's
-// LANES*4-byte slice of ROWS consecutive 1 KiB rounds; with LANES == 256 the
-// slices are contiguous and a stage is ONE bulk copy.
-template <int LANES_, int ROWS_, int STAGES_>
+// STAGES shared-memory stages of ROWS rounds each; a stage holds the CTA's
+// LANES*4-byte slice of ROWS consecutive 1 KiB rounds. TMA2D: stages are
+// filled by one 2-D tensor copy; otherwise (LANES == 256 only) by one 1-D
+// bulk copy of ROWS contiguous KiB.
+template <int LANES_, int ROWS_, int STAGES_, bool TMA2D_>
 struct HashCfg {
   static constexpr int LANES = LANES_;
   static constexpr int ROWS = ROWS_;
   static constexpr int STAGES = STAGES_;
+  static constexpr bool TMA2D = TMA2D_;
   static constexpr int GROUPS = 256 / LANES;
   static constexpr int SLICE = LANES * 4;
   static constexpr int STAGE_BYTES = ROWS * SLICE;
   static constexpr int SMEM = STAGE_BYTES * STAGES;
+  static_assert(TMA2D || LANES == 256, "1-D bulk stages need whole rounds");
 };
 
 // Run lanes [lane0, lane0 + LANES) of one segment; h is the lane's state.
 // Must be called by all threads of the CTA (uses __syncthreads).
 template <class C>
-__device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes, uint32_t lane0,
-                                               uint64_t h, uint8_t *stage, uint64_t *bars,
-                                               uint32_t &parity) {
+__device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes,
+                                               const CUtensorMap *map, uint32_t lane0, uint64_t h,
+                                               uint8_t *stage, uint64_t *bars, uint32_t &parity) {
   const int tid = threadIdx.x;
   const uint32_t lane = lane0 + tid;
   const uint64_t full_words = nbytes >> 2;
   const uint64_t rounds = full_words >> 8;
-  if (rounds > 0 && ((uintptr_t)p & 15) == 0) {
+  const bool fast = rounds > 0 && (C::TMA2D ? map != nullptr : ((uintptr_t)p & 15) == 0);
+  if (fast) {
     const uint64_t nst = (rounds + C::ROWS - 1) / C::ROWS;
-    const uint8_t *src0 = p + lane0 * 4;
-    // warp 0 fills stage slot `slot` with rounds [s*ROWS, s*ROWS + rows)
-    auto issue = [&](uint64_t s, int slot) {
-      const uint32_t rows = (uint32_t)min((uint64_t)C::ROWS, rounds - s * C::ROWS);
+    auto issue = [&](uint64_t s, int slot) {  // called by thread 0
       uint8_t *dst = stage + slot * C::STAGE_BYTES;
-      const uint8_t *src = src0 + s * C::ROWS * 1024;
-      if constexpr (C::LANES == 256) {
-        if (tid == 0) {
-          mbar_expect_tx(&bars[slot], rows * 1024);
-          bulk_g2s(dst, src, rows * 1024, &bars[slot]);
-        }
+      if constexpr (C::TMA2D) {
+        // out-of-range rows of the last box are zero-filled and still counted
+        mbar_expect_tx(&bars[slot], C::STAGE_BYTES);
+        tma_2d_g2s(dst, map, (int)lane0, (int)(s * C::ROWS), &bars[slot]);
       } else {
-        if (tid == 0) mbar_expect_tx(&bars[slot], rows * C::SLICE);
-        __syncwarp();
-        for (uint32_t i = tid; i < rows; i += 32)
-          bulk_g2s(dst + i * C::SLICE, src + (uint64_t)i * 1024, C::SLICE, &bars[slot]);
+        const uint32_t rows = (uint32_t)min((uint64_t)C::ROWS, rounds - s * C::ROWS);
+        mbar_expect_tx(&bars[slot], rows * 1024);
+        bulk_g2s(dst, p + s * C::ROWS * 1024, rows * 1024, &bars[slot]);
       }
     };
-    if (tid < 32)
+    if (tid == 0) {
+      if constexpr (C::TMA2D) tensormap_acquire(map);
       for (uint64_t s = 0; s < nst && s < (uint64_t)C::STAGES; ++s) issue(s, (int)s);
+    }
     for (uint64_t st = 0; st < nst; ++st) {
       const int slot = (int)(st % C::STAGES);
       mbar_wait(&bars[slot], (parity >> slot) & 1u);
@@ -170,7 +190,7 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
       }
       h = f.value();
       __syncthreads();  // every lane done with this slot before it is refilled
-      if (tid < 32 && st + C::STAGES < nst) issue(st + C::STAGES, slot);
+      if (tid == 0 && st + C::STAGES < nst) issue(st + C::STAGES, slot);
     }
   } else {
     for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
@@ -185,12 +205,12 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
 }
 
 // depth-8 tree over 256 lanes in shared memory (pairs (2j, 2j+1), lower is a);
-// any CTA size; returns the root in every thread
+// CTA size >= 64; returns the root in every thread
 __device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s) {
   const int tid = threadIdx.x, nt = blockDim.x;
   __syncthreads();
   for (int width = 128; width >= 1; width >>= 1) {
-    uint64_t v0 = 0, v1 = 0;  // nt >= 64 => at most 2 pairs per thread
+    uint64_t v0 = 0, v1 = 0;
     if (tid < width) v0 = (lane_s[2 * tid] ^ rotl27(lane_s[2 * tid + 1])) * kFnvPrime;
     if (tid + nt < width) v1 = (lane_s[2 * (tid + nt)] ^ rotl27(lane_s[2 * (tid + nt) + 1])) * kFnvPrime;
     __syncthreads();
@@ -210,8 +230,7 @@ __device__ __forceinline__ void init_bars(uint64_t *bars) {
   __syncthreads();
 }
 
-// Work item = (entry, lane group); entries arrive largest first, so the
-// longest chains start first. The last group of an entry to finish folds.
+// Work item = (entry, lane group); the last group of an entry folds.
 template <class C>
 __global__ void __launch_bounds__(C::LANES)
     simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *arrived) {
@@ -226,7 +245,7 @@ __global__ void __launch_bounds__(C::LANES)
     const uint32_t e = it / C::GROUPS, g = it % C::GROUPS;
     const HashEntry E = b.e[e];
     const uint32_t lane0 = g * C::LANES;
-    uint64_t h = hash_group<C>(E.ptr, E.nbytes, lane0, kFnvOffset, stage, bars, parity);
+    uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, parity);
     if constexpr (C::GROUPS == 1) {
       lane_s[threadIdx.x] = h;
       uint64_t root = tree_fold(lane_s);
@@ -249,16 +268,18 @@ __global__ void __launch_bounds__(C::LANES)
   }
 }
 
-// streaming update: grid = GROUPS CTAs, lane state in/out (no fold)
+// streaming update of one segment: grid = GROUPS CTAs, lane state in/out
 template <class C>
 __global__ void __launch_bounds__(C::LANES)
-    simplehash_update_kernel(uint64_t *state, const uint8_t *p, uint64_t nbytes) {
+    simplehash_update_kernel(uint64_t *state, const uint8_t *p, uint64_t nbytes,
+                             const __grid_constant__ CUtensorMap map, int have_map) {
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[C::STAGES];
   init_bars<C::STAGES>(bars);
   uint32_t parity = 0;
   const uint32_t lane = blockIdx.x * C::LANES + threadIdx.x;
-  uint64_t h = hash_group<C>(p, nbytes, blockIdx.x * C::LANES, state[lane], stage, bars, parity);
+  uint64_t h = hash_group<C>(p, nbytes, have_map ? &map : nullptr, blockIdx.x * C::LANES,
+                             state[lane], stage, bars, parity);
   state[lane] = h;
 }
 
@@ -272,21 +293,62 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
-// Variants (PCCLB_HASH_VARIANT selects one for experiments; 0 is the default)
-using HashV0 = HashCfg<256, 16, 12>;  // 192 KiB ring, 1 CTA/SM, 16 KiB copies
-using HashV1 = HashCfg<256, 16, 6>;   // 96 KiB ring, 2 CTAs/SM
-using HashV2 = HashCfg<128, 32, 6>;   // 2 CTAs per entry, 512 B slices
-using HashV3 = HashCfg<64, 64, 4>;    // 4 CTAs per entry, 256 B slices
-using HashV4 = HashCfg<128, 32, 12>;  // 2 CTAs per entry, 192 KiB ring
+// Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default)
+using HashV0 = HashCfg<128, 32, 6, true>;   // 2 CTAs/entry, 2-D TMA, 96 KiB ring
+using HashV1 = HashCfg<256, 16, 6, false>;  // 1 CTA/entry, 1-D bulk, 96 KiB ring
+using HashV2 = HashCfg<64, 64, 4, true>;    // 4 CTAs/entry, 2-D TMA, 64 KiB ring
+using HashV3 = HashCfg<128, 64, 3, true>;   // 2 CTAs/entry, 2-D TMA, 32 KiB stages
 
 int hash_variant() {
   static int v = [] {
     const char *e = getenv("PCCLB_HASH_VARIANT");
     int x = e ? atoi(e) : 0;
-    return (x < 0 || x > 4) ? 0 : x;
+    return (x < 0 || x > 3) ? 0 : x;
   }();
   return v;
 }
+
+// ---------------------------------------------------------------------------
+// host: tensor maps
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// [rounds x 256] u32 view of an entry, box LANES x ROWS; false if not encodable
+template <class C>
+static bool encode_map(CUtensorMap *m, const void *p, uint64_t nbytes) {
+  const uint64_t rounds = (nbytes >> 2) >> 8;
+  if (!rounds || (reinterpret_cast<uintptr_t>(p) & 15) || rounds >= (1ull << 31)) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {256, rounds};
+  cuuint64_t strides[1] = {1024};
+  cuuint32_t box[2] = {(cuuint32_t)C::LANES, (cuuint32_t)C::ROWS};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(p), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// pinned staging for tensor maps, reused once the previous upload finished
+struct MapStaging {
+  CUtensorMap *host = nullptr;
+  cudaEvent_t done = nullptr;
+  ~MapStaging() {
+    if (host) cudaFreeHost(host);
+    if (done) cudaEventDestroy(done);
+  }
+};
 
 template <class C>
 static int prepare_variant() {
@@ -308,7 +370,6 @@ static int prepare_hash_kernels() {
   if (!rc) rc = prepare_variant<HashV1>();
   if (!rc) rc = prepare_variant<HashV2>();
   if (!rc) rc = prepare_variant<HashV3>();
-  if (!rc) rc = prepare_variant<HashV4>();
   if (rc) return rc;
   if (dev >= 0 && dev < 64) done[dev] = true;
   return PCCLB_OK;
@@ -323,49 +384,70 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
                                                            C::LANES, C::SMEM));
   if (occ < 1) occ = 1;
   const uint32_t slots = (uint32_t)(sm_count() * occ);
-  // per-launch scratch: lane values + per-entry arrival counters
+  // per-launch device scratch: lane values, arrival counters, tensor maps
   const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
   const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  void *scratch = nullptr;
-  if (C::GROUPS > 1)
-    PCCLB_CUDA(cudaMallocAsync(&scratch, lanes_bytes + (size_t)m_max * sizeof(uint32_t), s));
-  uint64_t *lanes = static_cast<uint64_t *>(scratch);
-  uint32_t *arrived =
-      scratch ? reinterpret_cast<uint32_t *>(static_cast<char *>(scratch) + lanes_bytes) : nullptr;
+  const size_t cnt_bytes = ((size_t)m_max * sizeof(uint32_t) + 127) & ~size_t(127);
+  const size_t map_bytes = C::TMA2D ? (size_t)m_max * sizeof(CUtensorMap) : 0;
+  char *scratch = nullptr;
+  PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), lanes_bytes + cnt_bytes + map_bytes, s));
+  uint64_t *lanes = reinterpret_cast<uint64_t *>(scratch);
+  uint32_t *arrived = reinterpret_cast<uint32_t *>(scratch + lanes_bytes);
+  CUtensorMap *d_maps = reinterpret_cast<CUtensorMap *>(scratch + lanes_bytes + cnt_bytes);
   static thread_local HashBatch batch;
+  static thread_local MapStaging staging;
   int rc = PCCLB_OK;
   for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
-    uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
+    const uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
+    if (C::TMA2D) {
+      if (!staging.host) {
+        cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * kMaxBatch, cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&staging.done, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+          rc = cuda_status(e);
+          break;
+        }
+      } else {
+        cudaEventSynchronize(staging.done);  // previous upload out of the staging area
+      }
+    }
     batch.count = m;
     for (uint32_t i = 0; i < m; ++i) {
-      uint32_t k = order[base + i];
-      batch.e[i].ptr = static_cast<const uint8_t *>(h_ptrs[k]);
-      batch.e[i].nbytes = h_nbytes[k];
-      batch.e[i].out = d_out + k;
+      const uint32_t k = order[base + i];
+      HashEntry &E = batch.e[i];
+      E.ptr = static_cast<const uint8_t *>(h_ptrs[k]);
+      E.nbytes = h_nbytes[k];
+      E.out = d_out + k;
+      E.map = nullptr;
+      if (C::TMA2D && encode_map<C>(&staging.host[i], E.ptr, E.nbytes)) E.map = d_maps + i;
     }
-    if (arrived) {
-      cudaError_t e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
-      if (e != cudaSuccess) {
-        rc = cuda_status(e);
-        break;
-      }
+    cudaError_t e = cudaSuccess;
+    if (C::TMA2D) {
+      e = cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
+    }
+    if (e == cudaSuccess && C::GROUPS > 1) e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
+    if (e != cudaSuccess) {
+      rc = cuda_status(e);
+      break;
     }
     unsigned grid = std::min<uint32_t>(m * C::GROUPS, slots);
     simplehash_batch_kernel<C><<<grid, C::LANES, C::SMEM, s>>>(batch, lanes, arrived);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_status(e);
   }
-  if (scratch) {
-    cudaError_t e = cudaFreeAsync(scratch, s);
-    if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
-  }
+  cudaError_t e = cudaFreeAsync(scratch, s);
+  if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
   return rc;
 }
 
 template <class C>
 static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaStream_t s) {
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  int have = (C::TMA2D && encode_map<C>(&map, d, nbytes)) ? 1 : 0;
   simplehash_update_kernel<C><<<C::GROUPS, C::LANES, C::SMEM, s>>>(
-      state, static_cast<const uint8_t *>(d), nbytes);
+      state, static_cast<const uint8_t *>(d), nbytes, map, have);
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
 }
@@ -397,8 +479,6 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
       return launch_batches<HashV2>(order, h_ptrs, h_nbytes, count, d_out, s);
     case 3:
       return launch_batches<HashV3>(order, h_ptrs, h_nbytes, count, d_out, s);
-    case 4:
-      return launch_batches<HashV4>(order, h_ptrs, h_nbytes, count, d_out, s);
     default:
       return launch_batches<HashV0>(order, h_ptrs, h_nbytes, count, d_out, s);
   }
@@ -420,8 +500,7 @@ int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uint64_t nbyt
   if (nbytes == 0) return PCCLB_OK;
   int rc = prepare_hash_kernels();
   if (rc) return rc;
-  // a single chain set: the multi-CTA shape keeps more copies in flight
-  return launch_update<HashV4>(d_state, d_data, nbytes, as_stream(stream));
+  return launch_update<HashV0>(d_state, d_data, nbytes, as_stream(stream));
 }
 
 int pcclb_simplehash_final(const uint64_t *d_state, uint64_t total_nbytes, uint64_t *d_out,
