@@ -15,9 +15,9 @@
 // Mapping (default): an entry's 256 lanes are split over kGroups = 2 CTAs of
 // 128 threads (thread t = lane 128g + t), each on its own SM, so a lone large
 // entry runs at its chain bound. A CTA streams its 512-byte slice of every
-// 1 KiB round through a 6-stage shared-memory ring; each stage (32 rounds) is
+// 1 KiB round through a 3-stage shared-memory ring; each stage (64 rounds) is
 // ONE 2-D TMA copy (cp.async.bulk.tensor.2d, the entry viewed as a
-// [rounds x 256] u32 tensor, box 128 x 32) completing on an mbarrier.
+// [rounds x 256] u32 tensor, box 128 x 64) completing on an mbarrier.
 // Entries are dealt largest first, so the longest chains start first; the
 // last group of an entry to finish runs the tree fold.
 #include <cuda.h>
@@ -294,10 +294,13 @@ __global__ void __launch_bounds__(256)
 }
 
 // Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default)
-using HashV0 = HashCfg<128, 32, 6, true>;   // 2 CTAs/entry, 2-D TMA, 96 KiB ring
+// measured on B200 (config-4 layout / one 1.05 GB entry / 64 x 64 MiB):
+//   V0 13.4 ms / 84 GB/s / 4.90 TB/s    V1 22.0 ms / 47 GB/s / 2.61 TB/s
+//   V2 11.6 ms / 98 GB/s / 4.04 TB/s    V3 12.1 ms / 99 GB/s / 5.64 TB/s
+using HashV0 = HashCfg<128, 64, 3, true>;   // 2 CTAs/entry, 2-D TMA, 3 x 32 KiB stages
 using HashV1 = HashCfg<256, 16, 6, false>;  // 1 CTA/entry, 1-D bulk, 96 KiB ring
 using HashV2 = HashCfg<64, 64, 4, true>;    // 4 CTAs/entry, 2-D TMA, 64 KiB ring
-using HashV3 = HashCfg<128, 64, 3, true>;   // 2 CTAs/entry, 2-D TMA, 32 KiB stages
+using HashV3 = HashCfg<128, 32, 6, true>;   // 2 CTAs/entry, 2-D TMA, 6 x 16 KiB stages
 
 int hash_variant() {
   static int v = [] {
