@@ -303,6 +303,8 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     buf = torch.empty_like(src)
     esz = 4
     ring = DeviceRing(device=dev, capacity_bytes=16384 + n * esz + 4 * (n // world + 1) * esz + (1 << 20))
+    if not args.no_register:
+        ring.register(buf)  # one-time collective setup: peers read buf in place (zero-copy)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         buf.copy_(src)
@@ -359,6 +361,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
         "dtype": "f32",
         "config": {"workload": f"config{'3' if quantize else '2'}: in-place AVG all-reduce{' u8-quantized' if quantize else ''} of {S / 2**30:.3f} GiB fp32 per GPU over NVLink, W={world}",
                    "elements_per_gpu": n, "ring": list(range(world)), "algbw_GBps": round(algbw, 2),
+                   "buffer": "unregistered (staged copy-in)" if args.no_register else "registered once (DeviceRing.register, zero-copy reads)",
                    "busbw_definition": "algbw*2(W-1)/W", "l2": "1 GiB inputs > 126 MB L2"},
         "roofline": {"bound": "nvlink", "achieved": round(nvl_bytes / (ms_max * 1e-3) / 1e9, 1),
                      "peak": NVLINK_PEER_GBS, "unit": "GB/s",
@@ -473,6 +476,7 @@ def main():
     ap.add_argument("--elems", type=int, default=0, help="override elements per GPU (allreduce/quant/local)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-register", action="store_true", help="all-reduce: stage through the workspace instead of registering the buffer")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world_env = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

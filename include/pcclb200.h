@@ -172,6 +172,18 @@ PCCLB_API volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r);
 /* Element capacity for a dtype/quantize combination with this workspace. */
 PCCLB_API uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize);
 
+/* Caller-buffer registration (collective: every rank registers the same
+ * logical buffers in the same slot order). pcclb_ipc_handle gives the CUDA IPC
+ * handle of the allocation holding d_ptr and d_ptr's offset in it; after an
+ * out-of-band exchange, pcclb_ring_register maps every peer's buffer
+ * (handles: world x 64 bytes and offsets: world entries, ring-position order).
+ * All-reduces on a registered buffer read it in place over NVLink instead of
+ * staging a copy (the backup copy then overlaps the fold). */
+PCCLB_API int pcclb_ipc_handle(const void *d_ptr, void *handle64_out, uint64_t *offset_out);
+PCCLB_API int pcclb_ring_register(pcclb_ring *r, uint32_t slot, const void *local_ptr,
+                                  uint64_t nbytes, const void *handles, const uint64_t *offsets);
+PCCLB_API int pcclb_ring_deregister(pcclb_ring *r, uint32_t slot);
+
 /* run_all_reduce (collective.py:489-576) on this rank's buffer. `attempt` must
  * be identical on all ranks and strictly increasing per engine (the reference's
  * (tag, seq_nr) attempt identity, collective.py:343-356). `fault_at` >= 0

@@ -101,6 +101,9 @@ SIGNATURES = {
     ),
     "pcclb_ring_restore": (_I, [_P, _P, _U64, _I, _P]),
     "pcclb_ring_destroy": (None, [_P]),
+    "pcclb_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_U64)]),
+    "pcclb_ring_register": (_I, [_P, _U32, _P, _U64, _P, ctypes.POINTER(_U64)]),
+    "pcclb_ring_deregister": (_I, [_P, _U32]),
 }
 
 _lib = None

@@ -46,11 +46,15 @@
 // or on timeout; it then posts its own abort token to every peer. Later
 // kernels of the op see the status word and skip. The host reads the status
 // at the end and restores the caller's buffer from `in` (collective.py:568-574).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <new>
+#include <string>
 
 #include "common.cuh"
 #include "elementwise.cuh"
@@ -66,6 +70,7 @@ constexpr int kIpcThreads = 512;
 struct Signal {
   uint64_t arrive[kIpcMaxWorld];     // written by peer j: its latest barrier token
   uint64_t abort_tok[kIpcMaxWorld];  // written by peer j: attempt it aborted
+  uint64_t desc[kIpcMaxWorld];       // written by peer j: its buffer descriptor (barrier 0)
   pcclb_qmeta meta[2];               // reduce-step metas (by step parity)
   pcclb_qmeta meta_final;            // owned chunk's gather meta
   uint32_t status;                   // this rank's op status (0 = ok)
@@ -101,8 +106,10 @@ struct BarrierArgs {
   uint64_t token;
   uint64_t attempt;
   uint64_t timeout_ns;
+  uint64_t desc;   // this rank's buffer descriptor (registration slot/offset)
   uint32_t rank, world;
   uint32_t fault;  // 1: inject a local fault here
+  uint32_t check_desc;  // 1: every rank must publish the same descriptor
 };
 
 __global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__ BarrierArgs a) {
@@ -127,7 +134,10 @@ __global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__
     return;
   }
   __threadfence_system();
-  if (t < a.world && t != a.rank) st_release_sys(&a.peer[t]->arrive[a.rank], a.token);
+  if (t < a.world && t != a.rank) {
+    if (a.check_desc) *(volatile uint64_t *)&a.peer[t]->desc[a.rank] = a.desc;
+    st_release_sys(&a.peer[t]->arrive[a.rank], a.token);  // orders the desc store before it
+  }
   if (t != 0) return;
   const uint64_t t0 = globaltimer();
   uint32_t verdict = 0;
@@ -139,7 +149,13 @@ __global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__
       if (ld_acquire_sys(&me->abort_tok[j]) == a.attempt) verdict = PCCLB_EABORTED;
     }
     if (verdict) break;
-    if (all) break;
+    if (all) {
+      // SPMD check: zero-copy needs every rank on the same registered buffer
+      if (a.check_desc)
+        for (uint32_t j = 0; j < a.world; ++j)
+          if (j != a.rank && *(volatile uint64_t *)&me->desc[j] != a.desc) verdict = PCCLB_EINVAL;
+      break;
+    }
     if (a.host->abort) {
       verdict = PCCLB_EABORTED;
       break;
@@ -175,7 +191,7 @@ template <typename T>
 struct FoldArgs {
   const T *src[kIpcMaxWorld];  // src[k] = input of ring position (c + k) at chunk c
   T *dst0;                     // res
-  T *dst1;                     // caller buffer at chunk c
+  T *dst1;                     // caller buffer at chunk c (null: zero-copy mode)
   const Signal *mine;
   uint64_t n;
   uint32_t w;
@@ -194,13 +210,13 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
     for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.src[k][i], acc);
     acc = fin(acc);
     a.dst0[i] = acc;
-    a.dst1[i] = acc;
+    if (a.dst1) a.dst1[i] = acc;
   };
   if constexpr (VEC == 1) {
     for (uint64_t i = tid; i < a.n; i += nth) one(i);
   } else {
     constexpr int N = Pack16<T>::N;
-    uint64_t head = dpeel16<T>(a.dst1);
+    uint64_t head = dpeel16<T>(a.dst0);
     if (head > a.n) head = a.n;
     if (tid < head) one(tid);
     const uint64_t nv = (a.n - head) / N;
@@ -216,7 +232,7 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
 #pragma unroll
       for (int e = 0; e < N; ++e) acc.e[e] = fin(acc.e[e]);
       st16(a.dst0 + i, acc);
-      st16(a.dst1 + i, acc);
+      if (a.dst1) st16(a.dst1 + i, acc);
     }
     const uint64_t t0 = head + nv * N;
     if (tid < a.n - t0) one(t0 + tid);
@@ -341,8 +357,22 @@ struct PhaseTimer {
   }
 };
 
+// A caller buffer registered on every rank (collective; SPMD order): peers'
+// kernels read it in place, so the copy-in leaves the critical path.
+struct RegSlot {
+  bool used = false;
+  const char *local = nullptr;
+  uint64_t bytes = 0;
+  const char *peer[kIpcMaxWorld] = {};
+};
+constexpr int kMaxReg = 64;
+
 struct pcclb_ring {
   PhaseTimer timer;
+  RegSlot reg[kMaxReg];
+  std::map<std::string, char *> opened;  // peer allocations by IPC handle bytes
+  cudaStream_t side = nullptr;           // backup copies overlapping the fold
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int device;
   uint32_t rank, world;
   uint64_t capacity;
@@ -393,8 +423,11 @@ Layout layout_for(uint64_t n, uint32_t w, size_t esz, bool quant) {
 }
 
 int launch_barrier(pcclb_ring *r, uint64_t attempt, uint32_t index, int fault_at,
-                   const pcclb_range *check, uint64_t timeout_ns, cudaStream_t s) {
+                   const pcclb_range *check, uint64_t timeout_ns, cudaStream_t s,
+                   uint64_t desc = 0, bool check_desc = false) {
   BarrierArgs a{};
+  a.desc = desc;
+  a.check_desc = check_desc ? 1u : 0u;
   a.mine = sig_of(r->ws);
   for (uint32_t j = 0; j < r->world; ++j) a.peer[j] = sig_of(r->peer_ws[j]);
   a.host = r->host_dev;
@@ -414,6 +447,16 @@ unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
   return grid_for(n_vec, kIpcThreads, ctas_per_sm);
 }
 
+// registered slot containing [p, p + bytes), or -1
+int find_reg(const pcclb_ring *r, const void *p, uint64_t bytes) {
+  const char *c = static_cast<const char *>(p);
+  for (int i = 0; i < kMaxReg; ++i) {
+    const RegSlot &g = r->reg[i];
+    if (g.used && c >= g.local && c + bytes <= g.local + g.bytes) return i;
+  }
+  return -1;
+}
+
 template <typename T>
 int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt, int fault_at,
                     uint64_t timeout_ns, cudaStream_t s) {
@@ -424,26 +467,45 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const uint32_t own = (rank + 1) % w;  // collective.py:538
   const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
   Signal *me = sig_of(r->ws);
-  // copy-in: the caller's bytes become the backup and the peers' fold input
+  const int slot = find_reg(r, buf, n * sizeof(T));
+  const bool zero_copy = slot >= 0;
+  uint64_t desc = 0;
+  const T *inputs[kIpcMaxWorld];  // where each ring position's input lives
   r->timer.mark(s);
-  PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  if (zero_copy) {
+    // peers read the registered buffer in place; the backup (restore source)
+    // is copied on a side stream while the fold runs and joined before the
+    // gather overwrites the buffer
+    const uint64_t off = reinterpret_cast<const char *>(buf) - r->reg[slot].local;
+    desc = ((uint64_t)(slot + 1) << 40) | off;
+    for (uint32_t j = 0; j < w; ++j)
+      inputs[j] = reinterpret_cast<const T *>(j == rank ? (const char *)buf : r->reg[slot].peer[j] + off);
+    PCCLB_CUDA(cudaEventRecord(r->ev_fork, s));
+    PCCLB_CUDA(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
+    PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, r->side));
+    PCCLB_CUDA(cudaEventRecord(r->ev_join, r->side));
+  } else {
+    // copy-in: the caller's bytes become the backup and the peers' fold input
+    PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    for (uint32_t j = 0; j < w; ++j) inputs[j] = reinterpret_cast<const T *>(r->peer_ws[j] + L.in);
+  }
   r->timer.mark(s);
-  int rc = launch_barrier(r, attempt, 0, fault_at, nullptr, timeout_ns, s);
+  int rc = launch_barrier(r, attempt, 0, fault_at, nullptr, timeout_ns, s, desc, true);
   if (rc) return rc;
   r->timer.mark(s);
   if (own_n) {
     FoldArgs<T> f{};
-    for (uint32_t k = 0; k < w; ++k)
-      f.src[k] = reinterpret_cast<const T *>(r->peer_ws[(own + k) % w] + L.in) + own_lo;
+    for (uint32_t k = 0; k < w; ++k) f.src[k] = inputs[(own + k) % w] + own_lo;
     f.dst0 = reinterpret_cast<T *>(r->ws + res_off(L, own_lo, sizeof(T)));
-    f.dst1 = buf + own_lo;
+    f.dst1 = zero_copy ? nullptr : buf + own_lo;
     f.mine = me;
     f.n = own_n;
     f.w = w;
     f.avg = (op == PCCLB_AVG) ? w : 0;
     const unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
-    // peers' inputs and res share the chunk's sub-16-byte offset; buf must too
-    const bool vec = peel16<T>(f.dst1) == peel16<T>(f.src[0]) && peel16<T>(f.dst0) == peel16<T>(f.src[0]);
+    // every source and destination must share the sub-16-byte offset
+    bool vec = f.dst1 == nullptr || peel16<T>(f.dst1) == peel16<T>(f.dst0);
+    for (uint32_t k = 0; k < w; ++k) vec = vec && peel16<T>(f.src[k]) == peel16<T>(f.dst0);
 #define PCCLB_IPC_FOLD(OPC)                                                             \
   if (vec)                                                                              \
     ipc_fold_kernel<T, OPC, 16 / sizeof(T)><<<grid, kIpcThreads, 0, s>>>(f);            \
@@ -467,12 +529,13 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
   r->timer.mark(s);
+  if (zero_copy) PCCLB_CUDA(cudaStreamWaitEvent(s, r->ev_join, 0));
   GatherArgs g{};
   g.mine = me;
   uint32_t jobs = 0;
   uint64_t maxn = 0;
   for (uint32_t c = 0; c < w; ++c) {
-    if (c == own) continue;
+    if (c == own && !zero_copy) continue;  // already written by the fold
     const uint64_t cn = lo[2 * c + 1] - lo[2 * c];
     if (!cn) continue;
     const uint32_t owner = (c + w - 1) % w;
@@ -614,6 +677,9 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
     return cuda_status(e);
   }
   e = cudaMemset(r->ws, 0, kSignalBytes);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->host, sizeof(HostFlags), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->host_dev, r->host, 0);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, 64, cudaHostAllocDefault);
@@ -756,12 +822,75 @@ int pcclb_ring_restore(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, void *
   return PCCLB_OK;
 }
 
+int pcclb_ipc_handle(const void *d_ptr, void *handle64_out, uint64_t *offset_out) {
+  if (!d_ptr || !handle64_out || !offset_out) return PCCLB_EINVAL;
+  static PFN_cuMemGetAddressRange_v3020 range_fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  }();
+  if (!range_fn) return PCCLB_ECUDA;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, (CUdeviceptr)d_ptr) != CUDA_SUCCESS) return PCCLB_EINVAL;
+  cudaIpcMemHandle_t h;
+  PCCLB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  std::memcpy(handle64_out, &h, 64);
+  *offset_out = (uint64_t)((CUdeviceptr)d_ptr - base);
+  return PCCLB_OK;
+}
+
+int pcclb_ring_register(pcclb_ring *r, uint32_t slot, const void *local_ptr, uint64_t nbytes,
+                        const void *handles, const uint64_t *offsets) {
+  if (!r || slot >= (uint32_t)kMaxReg || !local_ptr || !handles || !offsets) return PCCLB_EINVAL;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  RegSlot g;
+  g.local = static_cast<const char *>(local_ptr);
+  g.bytes = nbytes;
+  for (uint32_t j = 0; j < r->world; ++j) {
+    if (j == r->rank) {
+      g.peer[j] = g.local;
+      continue;
+    }
+    std::string key(static_cast<const char *>(handles) + 64 * (size_t)j, 64);
+    auto it = r->opened.find(key);
+    char *base = nullptr;
+    if (it != r->opened.end()) {
+      base = it->second;
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, key.data(), 64);
+      void *p = nullptr;
+      PCCLB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      base = static_cast<char *>(p);
+      r->opened.emplace(key, base);
+    }
+    g.peer[j] = base + offsets[j];
+  }
+  g.used = true;
+  r->reg[slot] = g;
+  return PCCLB_OK;
+}
+
+int pcclb_ring_deregister(pcclb_ring *r, uint32_t slot) {
+  if (!r || slot >= (uint32_t)kMaxReg) return PCCLB_EINVAL;
+  r->reg[slot] = RegSlot();  // mappings stay cached until destroy
+  return PCCLB_OK;
+}
+
 void pcclb_ring_destroy(pcclb_ring *r) {
   if (!r) return;
   cudaSetDevice(r->device);
   cudaDeviceSynchronize();
   for (uint32_t j = 0; j < r->world; ++j)
     if (j != r->rank && r->imported[j] && r->peer_ws[j]) cudaIpcCloseMemHandle(r->peer_ws[j]);
+  for (auto &kv : r->opened) cudaIpcCloseMemHandle(kv.second);
+  if (r->side) cudaStreamDestroy(r->side);
+  if (r->ev_fork) cudaEventDestroy(r->ev_fork);
+  if (r->ev_join) cudaEventDestroy(r->ev_join);
   if (r->ws) cudaFree(r->ws);
   if (r->host) cudaFreeHost((void *)r->host);
   if (r->status_host) cudaFreeHost(r->status_host);

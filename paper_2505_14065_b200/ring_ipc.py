@@ -70,6 +70,7 @@ class DeviceRing:
         self._attempt = 0
         self._handle = None
         self._capacity = 0
+        self._registered: dict[int, torch.Tensor] = {}  # slot -> tensor (kept alive)
         self._create(capacity_bytes)
 
     # -- workspace lifecycle (collective: every rank calls in the same order) --
@@ -91,6 +92,8 @@ class DeviceRing:
             buf = ctypes.create_string_buffer(handles[grank], 64)
             check(lib().pcclb_ring_import(h, pos, buf), f"ring_import(peer {pos})")
         self._abort = lib().pcclb_ring_abort_word(h)
+        for slot, t in sorted(self._registered.items()):
+            self._register_slot(slot, t)
 
     def _destroy(self) -> None:
         if self._handle is not None:
@@ -113,6 +116,37 @@ class DeviceRing:
         esz = torch.tensor([], dtype=dtype).element_size()
         need = 16384 + n * esz + 4 * ((n + self.world - 1) // self.world) * max(esz, 1) + 4096
         self._create(int(need * 1.05))
+
+    # -- caller-buffer registration (collective, SPMD order) --
+    def register(self, tensor: torch.Tensor) -> int:
+        """Register a CUDA tensor on every rank (all ranks call with their
+        counterpart tensor, in the same order). All-reduces on (slices of) it
+        then read it in place over NVLink. Returns the registration slot; the
+        engine keeps the tensor alive until ``deregister``."""
+        if not isinstance(tensor, torch.Tensor) or not tensor.is_cuda or not tensor.is_contiguous():
+            raise UsageError("register needs a contiguous CUDA tensor")
+        slot = 0
+        while slot in self._registered:
+            slot += 1
+        self._register_slot(slot, tensor)
+        self._registered[slot] = tensor
+        return slot
+
+    def _register_slot(self, slot: int, tensor: torch.Tensor) -> None:
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64()
+        check(lib().pcclb_ipc_handle(tensor.data_ptr(), handle, ctypes.byref(off)), "ipc_handle")
+        allv = exchange_bytes(bytes(handle.raw) + int(off.value).to_bytes(8, "little"), self.group)
+        handles = b"".join(allv[g][:64] for g in self.ring)
+        offsets = (ctypes.c_uint64 * self.world)(*[int.from_bytes(allv[g][64:72], "little") for g in self.ring])
+        hbuf = ctypes.create_string_buffer(handles, len(handles))
+        nbytes = tensor.numel() * tensor.element_size()
+        check(lib().pcclb_ring_register(self._handle, slot, tensor.data_ptr(), nbytes, hbuf, offsets), "ring_register")
+
+    def deregister(self, slot: int) -> None:
+        if slot in self._registered:
+            check(lib().pcclb_ring_deregister(self._handle, slot), "ring_deregister")
+            del self._registered[slot]
 
     # -- control-plane hooks --
     def signal_abort(self) -> None:
@@ -144,6 +178,9 @@ class DeviceRing:
             self._handle, buffer.data_ptr(), n, DTYPE_CODE[buffer.dtype], op.code, int(quantize),
             self._attempt, fault_at, self.timeout_s, ctypes.byref(stats), s,
         )
+        if rc == _native.PCCLB_EINVAL:
+            raise UsageError("ring all-reduce rejected its arguments (ranks must agree on size, dtype, "
+                             "op, quantization and buffer registration)")
         if rc in _STATUS_REASON:
             reason, source = _STATUS_REASON[rc]
             raise CollectiveAborted(reason, source=source)

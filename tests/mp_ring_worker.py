@@ -125,6 +125,43 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             ring.run_all_reduce(buf, "max")
             ring.restore(buf)
             check("veto restore", buf.cpu().numpy().tobytes() == mine.tobytes())
+        if "registered" in scenarios:
+            # zero-copy path: peers read the registered buffer in place
+            n = (1 << 22) + 5
+            inputs = [np.random.default_rng(300 + p).normal(0, 2, n).astype(np.float32) for p in range(world)]
+            reg = torch.empty(n + 64, dtype=torch.float32, device=dev)
+            ring.register(reg)
+            for lo_off, cnt, quant, op in ((0, n, False, "avg"), (7, n - 100, False, "sum"), (3, n - 9, True, "avg"), (0, 1000, False, "max")):
+                view = reg[lo_off : lo_off + cnt]
+                mine = inputs[ring.position][:cnt]
+                view.copy_(torch.from_numpy(mine))
+                ring.run_all_reduce(view, op, quantize=quant)
+                want = oring.ring_allreduce_chunkwise([x[:cnt] for x in inputs], oring.ReduceOp[op.upper()], quantize=quant)
+                check(f"registered off={lo_off} n={cnt} q={quant} {op}", view.cpu().numpy().tobytes() == want.tobytes())
+            # abort atomicity in zero-copy mode
+            for k in range(2):
+                view = reg[:n]
+                mine = inputs[ring.position]
+                view.copy_(torch.from_numpy(mine))
+                aborted = False
+                try:
+                    ring.run_all_reduce(view, "sum", fault_at=k if rank == k % world else -1)
+                except CollectiveAborted:
+                    aborted = True
+                check(f"registered fault at={k}: aborted", aborted)
+                check(f"registered fault at={k}: restored", view.cpu().numpy().tobytes() == mine.tobytes())
+            # one rank unregistered -> every rank rejects the op, buffers intact
+            other = torch.from_numpy(inputs[ring.position].copy()).to(dev)
+            target = other if rank == 0 else reg[:n]
+            target.copy_(torch.from_numpy(inputs[ring.position]))
+            rejected = False
+            try:
+                ring.run_all_reduce(target, "sum")
+            except Exception as e:  # noqa: BLE001
+                rejected = "registration" in str(e)
+            check("registration mismatch rejected", rejected)
+            check("registration mismatch intact", target.cpu().numpy().tobytes() == inputs[ring.position].tobytes())
+            ring.deregister(0)
         if "large" in scenarios:
             n = (1 << 24) + 3
             for quant in (False, True):
@@ -163,5 +200,5 @@ if __name__ == "__main__":
     import torch.multiprocessing as mp
 
     world, port, outdir = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-    scenarios = sys.argv[4:] or ["golden", "faults", "large"]
+    scenarios = sys.argv[4:] or ["golden", "faults", "registered", "large"]
     mp.spawn(_entry, args=(world, port, outdir, scenarios), nprocs=world, join=True)
