@@ -247,10 +247,58 @@ struct GatherArgs {
   const void *src[kIpcMaxWorld];       // plain: owner's res; quantized: owner's codesF
   const pcclb_qmeta *meta[kIpcMaxWorld];  // quantized: owner's meta_final
   void *dst[kIpcMaxWorld];             // caller buffer at that chunk
+  void *bak[kIpcMaxWorld];             // plain, zero-copy: save the old bytes here first
   uint64_t n[kIpcMaxWorld];
   const Signal *mine;
   uint32_t avg;
 };
+
+// dst <- src, optionally saving dst's old contents to bak (fused backup:
+// the gather is NVLink-bound, so the extra local read+write is free)
+template <typename T, bool BAK>
+__device__ __forceinline__ void gather_copy(const T *src, T *dst, T *bak, uint64_t n) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int N = Pack16<T>::N;
+  auto one = [&](uint64_t i) {
+    if (BAK) bak[i] = dst[i];
+    dst[i] = src[i];
+  };
+  uint64_t head = dpeel16<T>(dst);
+  if (head > n) head = n;
+  const bool vec = dpeel16<T>(src) == head && (!BAK || dpeel16<T>(bak) == head);
+  if (!vec) {
+    for (uint64_t i = tid; i < n; i += nth) one(i);
+    return;
+  }
+  if (tid < head) one(tid);
+  const uint64_t nv = (n - head) / N;
+  const T *s0 = src + head;
+  T *d0 = dst + head;
+  T *b0 = BAK ? bak + head : nullptr;
+  uint64_t v = tid;
+  constexpr int U = 4;
+  for (; v + (U - 1) * nth < nv; v += U * nth) {
+    Pack16<T> x[U], o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = ld16(s0 + (v + u * nth) * N);
+    if (BAK) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) o[u] = ld16(d0 + (v + u * nth) * N);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st16(b0 + (v + u * nth) * N, o[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) st16(d0 + (v + u * nth) * N, x[u]);
+  }
+  for (; v < nv; v += nth) {
+    Pack16<T> x = ld16(s0 + v * N);
+    if (BAK) st16(b0 + v * N, ld16(d0 + v * N));
+    st16(d0 + v * N, x);
+  }
+  const uint64_t t0 = head + nv * N;
+  if (tid < n - t0) one(t0 + tid);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __grid_constant__ GatherArgs a) {
@@ -258,31 +306,10 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __g
   const uint32_t j = blockIdx.y;
   const T *src = static_cast<const T *>(a.src[j]);
   T *dst = static_cast<T *>(a.dst[j]);
-  const uint64_t n = a.n[j];
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-  constexpr int N = Pack16<T>::N;
-  uint64_t head = dpeel16<T>(dst);
-  if (head > n) head = n;
-  const bool vec = dpeel16<T>(src) == head;
-  if (!vec) {
-    for (uint64_t i = tid; i < n; i += nth) dst[i] = src[i];
-    return;
-  }
-  if (tid < head) dst[tid] = src[tid];
-  const uint64_t nv = (n - head) / N;
-  uint64_t v = tid;
-  for (; v + 3 * nth < nv; v += 4 * nth) {
-    Pack16<T> x0 = ld16(src + head + v * N), x1 = ld16(src + head + (v + nth) * N);
-    Pack16<T> x2 = ld16(src + head + (v + 2 * nth) * N), x3 = ld16(src + head + (v + 3 * nth) * N);
-    st16(dst + head + v * N, x0);
-    st16(dst + head + (v + nth) * N, x1);
-    st16(dst + head + (v + 2 * nth) * N, x2);
-    st16(dst + head + (v + 3 * nth) * N, x3);
-  }
-  for (; v < nv; v += nth) st16(dst + head + v * N, ld16(src + head + v * N));
-  const uint64_t t0 = head + nv * N;
-  if (tid < n - t0) dst[t0 + tid] = src[t0 + tid];
+  if (a.bak[j])
+    gather_copy<T, true>(src, dst, static_cast<T *>(a.bak[j]), a.n[j]);
+  else
+    gather_copy<T, false>(src, dst, nullptr, a.n[j]);
 }
 
 __global__ void __launch_bounds__(kIpcThreads) ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a) {
@@ -371,8 +398,7 @@ struct pcclb_ring {
   PhaseTimer timer;
   RegSlot reg[kMaxReg];
   std::map<std::string, char *> opened;  // peer allocations by IPC handle bytes
-  cudaStream_t side = nullptr;           // backup copies overlapping the fold
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool last_zero_copy = false;           // last op read the caller buffer in place
   int device;
   uint32_t rank, world;
   uint64_t capacity;
@@ -469,21 +495,19 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   Signal *me = sig_of(r->ws);
   const int slot = find_reg(r, buf, n * sizeof(T));
   const bool zero_copy = slot >= 0;
+  r->last_zero_copy = zero_copy;
   uint64_t desc = 0;
   const T *inputs[kIpcMaxWorld];  // where each ring position's input lives
   r->timer.mark(s);
   if (zero_copy) {
-    // peers read the registered buffer in place; the backup (restore source)
-    // is copied on a side stream while the fold runs and joined before the
-    // gather overwrites the buffer
+    // peers read the registered buffer in place. Nothing writes the buffer
+    // before barrier 1, and no abort point follows it, so engine aborts need
+    // no backup; the gather saves the old bytes into `in` as it overwrites
+    // them, keeping pcclb_ring_restore (completion veto) available.
     const uint64_t off = reinterpret_cast<const char *>(buf) - r->reg[slot].local;
     desc = ((uint64_t)(slot + 1) << 40) | off;
     for (uint32_t j = 0; j < w; ++j)
       inputs[j] = reinterpret_cast<const T *>(j == rank ? (const char *)buf : r->reg[slot].peer[j] + off);
-    PCCLB_CUDA(cudaEventRecord(r->ev_fork, s));
-    PCCLB_CUDA(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
-    PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, r->side));
-    PCCLB_CUDA(cudaEventRecord(r->ev_join, r->side));
   } else {
     // copy-in: the caller's bytes become the backup and the peers' fold input
     PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
@@ -529,7 +553,6 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
   r->timer.mark(s);
-  if (zero_copy) PCCLB_CUDA(cudaStreamWaitEvent(s, r->ev_join, 0));
   GatherArgs g{};
   g.mine = me;
   uint32_t jobs = 0;
@@ -541,6 +564,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     const uint32_t owner = (c + w - 1) % w;
     g.src[jobs] = r->peer_ws[owner] + res_off(L, lo[2 * c], sizeof(T));
     g.dst[jobs] = buf + lo[2 * c];
+    g.bak[jobs] = zero_copy ? r->ws + L.in + lo[2 * c] * sizeof(T) : nullptr;
     g.n[jobs] = cn;
     maxn = cn > maxn ? cn : maxn;
     ++jobs;
@@ -677,9 +701,6 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
     return cuda_status(e);
   }
   e = cudaMemset(r->ws, 0, kSignalBytes);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->host, sizeof(HostFlags), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->host_dev, r->host, 0);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, 64, cudaHostAllocDefault);
@@ -794,7 +815,6 @@ int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int 
   else
     rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
   if (rc) return rc;
-  r->have_backup = true;
   PCCLB_CUDA(cudaMemcpyAsync(r->status_host, &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   PCCLB_CUDA(cudaStreamSynchronize(s));
   if (out_stats) {
@@ -806,10 +826,15 @@ int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int 
     }
   }
   const uint32_t st = *r->status_host;
+  // zero-copy ops never write the buffer before their last barrier, so an
+  // aborted one left it untouched; staged ops restore from the copy-in
+  const bool zc = !quantize && r->last_zero_copy;
+  r->have_backup = (st == 0) || !zc;
   if (st == 0) return PCCLB_OK;
-  // restore the caller's bytes (collective.py:568-574)
-  PCCLB_CUDA(cudaMemcpyAsync(d_buf, r->ws + kSignalBytes, n * esz, cudaMemcpyDeviceToDevice, s));
-  PCCLB_CUDA(cudaStreamSynchronize(s));
+  if (!zc) {  // restore the caller's bytes (collective.py:568-574)
+    PCCLB_CUDA(cudaMemcpyAsync(d_buf, r->ws + kSignalBytes, n * esz, cudaMemcpyDeviceToDevice, s));
+    PCCLB_CUDA(cudaStreamSynchronize(s));
+  }
   return (int)st;
 }
 
@@ -888,9 +913,6 @@ void pcclb_ring_destroy(pcclb_ring *r) {
   for (uint32_t j = 0; j < r->world; ++j)
     if (j != r->rank && r->imported[j] && r->peer_ws[j]) cudaIpcCloseMemHandle(r->peer_ws[j]);
   for (auto &kv : r->opened) cudaIpcCloseMemHandle(kv.second);
-  if (r->side) cudaStreamDestroy(r->side);
-  if (r->ev_fork) cudaEventDestroy(r->ev_fork);
-  if (r->ev_join) cudaEventDestroy(r->ev_join);
   if (r->ws) cudaFree(r->ws);
   if (r->host) cudaFreeHost((void *)r->host);
   if (r->status_host) cudaFreeHost(r->status_host);

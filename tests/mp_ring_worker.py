@@ -150,6 +150,13 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                     aborted = True
                 check(f"registered fault at={k}: aborted", aborted)
                 check(f"registered fault at={k}: restored", view.cpu().numpy().tobytes() == mine.tobytes())
+            # completion veto restore in zero-copy mode (backup fused into the gather)
+            view = reg[5 : 5 + n - 50]
+            mine = inputs[ring.position][: n - 50]
+            view.copy_(torch.from_numpy(mine))
+            ring.run_all_reduce(view, "avg")
+            ring.restore(view)
+            check("registered veto restore", view.cpu().numpy().tobytes() == mine.tobytes())
             # one rank unregistered -> every rank rejects the op, buffers intact
             other = torch.from_numpy(inputs[ring.position].copy()).to(dev)
             target = other if rank == 0 else reg[:n]
