@@ -196,13 +196,46 @@ struct FoldArgs {
   uint64_t n;
   uint32_t w;
   uint32_t avg;
+  // zero-copy mode: CTAs [fold_ctas, gridDim.x) copy the caller buffer into
+  // the backup meanwhile (the fold is NVLink-bound; local HBM has room)
+  uint32_t fold_ctas;
+  const void *bak_src;
+  void *bak_dst;
+  uint64_t bak_bytes;
 };
+
+// plain 16-byte-vector copy by a subset of CTAs (both pointers 16B-aligned)
+__device__ __forceinline__ void cta_range_copy(const void *src, void *dst, uint64_t bytes,
+                                               uint32_t cta, uint32_t nctas) {
+  const uint4 *s4 = static_cast<const uint4 *>(src);
+  uint4 *d4 = static_cast<uint4 *>(dst);
+  const uint64_t nv = bytes / 16;
+  const uint64_t tid = (uint64_t)cta * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)nctas * blockDim.x;
+  uint64_t v = tid;
+  for (; v + 3 * nth < nv; v += 4 * nth) {
+    uint4 a = __ldcs(s4 + v), b = __ldcs(s4 + v + nth), c = __ldcs(s4 + v + 2 * nth), d = __ldcs(s4 + v + 3 * nth);
+    __stcs(d4 + v, a);
+    __stcs(d4 + v + nth, b);
+    __stcs(d4 + v + 2 * nth, c);
+    __stcs(d4 + v + 3 * nth, d);
+  }
+  for (; v < nv; v += nth) __stcs(d4 + v, __ldcs(s4 + v));
+  const uint64_t t0 = nv * 16;
+  const char *sc = static_cast<const char *>(src);
+  char *dc = static_cast<char *>(dst);
+  if (tid < bytes - t0) dc[t0 + tid] = sc[t0 + tid];
+}
 
 template <typename T, int OP, int VEC>
 __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
   if (op_failed(a.mine)) return;
+  if (blockIdx.x >= a.fold_ctas) {
+    cta_range_copy(a.bak_src, a.bak_dst, a.bak_bytes, blockIdx.x - a.fold_ctas, gridDim.x - a.fold_ctas);
+    return;
+  }
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nth = (uint64_t)a.fold_ctas * blockDim.x;
   const uint32_t w = a.w;
   auto fin = [&](T v) { return a.avg ? x86_div(v, (T)a.avg) : v; };
   auto one = [&](uint64_t i) {
@@ -502,8 +535,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   if (zero_copy) {
     // peers read the registered buffer in place. Nothing writes the buffer
     // before barrier 1, and no abort point follows it, so engine aborts need
-    // no backup; the gather saves the old bytes into `in` as it overwrites
-    // them, keeping pcclb_ring_restore (completion veto) available.
+    // no backup; the fold launch copies it into `in` on spare CTAs (local HBM
+    // is idle while the fold waits on NVLink), keeping pcclb_ring_restore
+    // (completion veto) available.
     const uint64_t off = reinterpret_cast<const char *>(buf) - r->reg[slot].local;
     desc = ((uint64_t)(slot + 1) << 40) | off;
     for (uint32_t j = 0; j < w; ++j)
@@ -526,7 +560,16 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     f.n = own_n;
     f.w = w;
     f.avg = (op == PCCLB_AVG) ? w : 0;
-    const unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
+    unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
+    f.fold_ctas = grid;
+    if (zero_copy) {
+      // backup: the caller's buffer (16B-aligned run) -> in; see FoldArgs
+      f.bak_src = buf;
+      f.bak_dst = r->ws + L.in;
+      f.bak_bytes = n * sizeof(T);
+      if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0) grid += (unsigned)sm_count();
+      else f.fold_ctas = grid;  // unaligned: copied below instead
+    }
     // every source and destination must share the sub-16-byte offset
     bool vec = f.dst1 == nullptr || peel16<T>(f.dst1) == peel16<T>(f.dst0);
     for (uint32_t k = 0; k < w; ++k) vec = vec && peel16<T>(f.src[k]) == peel16<T>(f.dst0);
@@ -549,6 +592,8 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
 #undef PCCLB_IPC_FOLD
     PCCLB_LAUNCH_CHECK();
   }
+  if (zero_copy && (own_n == 0 || (reinterpret_cast<uintptr_t>(buf) & 15) != 0))
+    PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
   r->timer.mark(s);
   rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
@@ -564,7 +609,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     const uint32_t owner = (c + w - 1) % w;
     g.src[jobs] = r->peer_ws[owner] + res_off(L, lo[2 * c], sizeof(T));
     g.dst[jobs] = buf + lo[2 * c];
-    g.bak[jobs] = zero_copy ? r->ws + L.in + lo[2 * c] * sizeof(T) : nullptr;
+    g.bak[jobs] = nullptr;
     g.n[jobs] = cn;
     maxn = cn > maxn ? cn : maxn;
     ++jobs;

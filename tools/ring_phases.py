@@ -18,6 +18,8 @@ quant = len(sys.argv) > 2 and sys.argv[2] == "quant"
 dev = torch.device("cuda", local)
 buf = torch.randn(n, device=dev) * (1e-2 if quant else 1)
 ring = DeviceRing(device=dev, capacity_bytes=16384 + n * 4 + 4 * (n // world + 1) * 4 + (1 << 20))
+if os.environ.get("REGISTER", "1") == "1":
+    ring.register(buf)
 rows = []
 for i in range(8):
     st = ring.run_all_reduce(buf, "avg", quantize=quant)
