@@ -193,6 +193,15 @@ PCCLB_API int pcclb_ring_deregister(pcclb_ring *r, uint32_t slot);
 PCCLB_API int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op,
                          int quantize, uint64_t attempt, int fault_at, double timeout_s,
                          pcclb_stats *out_stats, void *stream);
+/* Asynchronous form (all_reduce_async / await_async_reduce, client.py:802-843):
+ * enqueue returns a ticket once every kernel of the op is on `stream`; wait
+ * blocks until it resolves and returns the same statuses as
+ * pcclb_ring_allreduce (which is enqueue + wait). Up to 64 ops may be
+ * outstanding; ops on one stream run in order. */
+PCCLB_API int pcclb_ring_enqueue(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op,
+                                 int quantize, uint64_t attempt, int fault_at, double timeout_s,
+                                 void *stream, uint32_t *ticket_out);
+PCCLB_API int pcclb_ring_wait(pcclb_ring *r, uint32_t ticket, pcclb_stats *out_stats);
 /* Restore the last op's input (completion-vote veto, client.py:973-983).
  * Valid until the next pcclb_ring_allreduce on this engine. */
 PCCLB_API int pcclb_ring_restore(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, void *stream);

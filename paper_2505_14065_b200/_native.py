@@ -100,6 +100,11 @@ SIGNATURES = {
         [_P, _P, _U64, _I, _I, _I, _U64, _I, ctypes.c_double, ctypes.POINTER(Stats), _P],
     ),
     "pcclb_ring_restore": (_I, [_P, _P, _U64, _I, _P]),
+    "pcclb_ring_enqueue": (
+        _I,
+        [_P, _P, _U64, _I, _I, _I, _U64, _I, ctypes.c_double, _P, ctypes.POINTER(_U32)],
+    ),
+    "pcclb_ring_wait": (_I, [_P, _U32, ctypes.POINTER(Stats)]),
     "pcclb_ring_destroy": (None, [_P]),
     "pcclb_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_U64)]),
     "pcclb_ring_register": (_I, [_P, _U32, _P, _U64, _P, ctypes.POINTER(_U64)]),

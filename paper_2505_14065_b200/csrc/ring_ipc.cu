@@ -427,6 +427,20 @@ struct RegSlot {
 };
 constexpr int kMaxReg = 64;
 
+// one enqueued all-reduce (pcclb_ring_enqueue .. pcclb_ring_wait)
+constexpr int kMaxOps = 64;
+struct OpRec {
+  bool pending = false;
+  bool quantize = false;
+  bool zero_copy = false;
+  bool timed = false;
+  void *buf = nullptr;
+  uint64_t n = 0;
+  int dtype = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
 struct pcclb_ring {
   PhaseTimer timer;
   RegSlot reg[kMaxReg];
@@ -440,7 +454,10 @@ struct pcclb_ring {
   bool imported[kIpcMaxWorld];
   HostFlags *host;                 // host-mapped
   HostFlags *host_dev;             // device alias
-  uint32_t *status_host;           // pinned status readback
+  uint32_t *status_host;           // pinned status readback, one slot per op record
+  OpRec ops[kMaxOps];
+  cudaEvent_t op_events[kMaxOps];
+  uint32_t next_ticket = 0;
   uint64_t last_n;
   int last_dtype;
   bool have_backup;
@@ -748,7 +765,9 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
   e = cudaMemset(r->ws, 0, kSignalBytes);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->host, sizeof(HostFlags), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->host_dev, r->host, 0);
-  if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, 64, cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, sizeof(uint32_t) * kMaxOps, cudaHostAllocDefault);
+  for (int i = 0; i < kMaxOps && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&r->op_events[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     pcclb_ring_destroy(r);
@@ -808,79 +827,111 @@ uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize) {
   return lo;
 }
 
-int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op, int quantize,
-                         uint64_t attempt, int fault_at, double timeout_s, pcclb_stats *out_stats,
-                         void *stream) {
-  if (!r || !valid_dtype(dtype) || !valid_op(op) || (n && !d_buf)) return PCCLB_EINVAL;
+int pcclb_ring_enqueue(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op, int quantize,
+                       uint64_t attempt, int fault_at, double timeout_s, void *stream,
+                       uint32_t *ticket_out) {
+  if (!r || !ticket_out || !valid_dtype(dtype) || !valid_op(op) || (n && !d_buf)) return PCCLB_EINVAL;
   if (quantize && dtype != PCCLB_F32) return PCCLB_EINVAL;  // client.py:818-819
   if (attempt == 0 || attempt >= (1ull << 55)) return PCCLB_EINVAL;
   for (uint32_t j = 0; j < r->world; ++j)
     if (!r->imported[j]) return PCCLB_EINVAL;
   const size_t esz = dtype_size(dtype);
   if (layout_for(n, r->world, esz, quantize != 0).end > r->capacity) return PCCLB_ENOMEM;
+  const uint32_t t = r->next_ticket % kMaxOps;
+  OpRec &o = r->ops[t];
+  if (o.pending) return PCCLB_EINVAL;  // too many outstanding ops
   PCCLB_CUDA(cudaSetDevice(r->device));
   cudaStream_t s = as_stream(stream);
   const uint32_t w = r->world;
+  o = OpRec{};
+  o.done = r->op_events[t];
+  o.buf = d_buf;
+  o.n = n;
+  o.dtype = dtype;
+  o.quantize = quantize != 0;
+  o.stream = s;
+  o.timed = r->timer.on;
+  r->status_host[t] = 0;
+  if (w == 1) {  // client.py:896-900
+    int rc = pcclb_finalize(d_buf, n, dtype, op, 1, stream);
+    if (rc) return rc;
+  } else {
+    Signal *me = sig_of(r->ws);
+    r->timer.n = 0;
+    PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
+    const uint64_t timeout_ns = (uint64_t)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
+    int rc;
+    if (quantize)
+      rc = quant_allreduce(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+    else if (dtype == PCCLB_F32)
+      rc = plain_allreduce<float>(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+    else
+      rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+    if (rc) return rc;
+    o.zero_copy = !quantize && r->last_zero_copy;
+    PCCLB_CUDA(cudaMemcpyAsync(&r->status_host[t], &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  }
+  PCCLB_CUDA(cudaEventRecord(o.done, s));
+  o.pending = true;
+  r->next_ticket++;
+  *ticket_out = t;
+  return PCCLB_OK;
+}
+
+int pcclb_ring_wait(pcclb_ring *r, uint32_t ticket, pcclb_stats *out_stats) {
+  if (!r || ticket >= (uint32_t)kMaxOps || !r->ops[ticket].pending) return PCCLB_EINVAL;
+  OpRec &o = r->ops[ticket];
+  o.pending = false;
+  PCCLB_CUDA(cudaSetDevice(r->device));
+  PCCLB_CUDA(cudaEventSynchronize(o.done));
+  const uint32_t w = r->world;
+  const size_t esz = dtype_size(o.dtype);
   if (out_stats) {
     // algorithmic payload per peer: 2(W-1)/W * N * elem (test_ring_engine.py:99-108)
     uint64_t lo[2 * kIpcMaxWorld];
-    pcclb_chunk_bounds(n, w, lo);
+    pcclb_chunk_bounds(o.n, w, lo);
     uint64_t tx = 0;
-    const uint64_t ebytes = quantize ? 1 : esz;
-    for (uint32_t step = 0; step + 1 < w; ++step) {
+    const uint64_t ebytes = o.quantize ? 1 : esz;
+    for (uint32_t step = 0; w > 1 && step + 1 < w; ++step) {
       uint32_t c = (r->rank + w - step % w) % w;
       tx += (lo[2 * c + 1] - lo[2 * c]) * ebytes;
     }
     uint32_t cur = (r->rank + 1) % w;
-    for (uint32_t step = 0; step + 1 < w; ++step) {
+    for (uint32_t step = 0; w > 1 && step + 1 < w; ++step) {
       tx += (lo[2 * cur + 1] - lo[2 * cur]) * ebytes;
       cur = (cur + w - 1) % w;
     }
     out_stats->tx_payload_bytes = tx;
     out_stats->rx_payload_bytes = tx;
-  }
-  r->last_n = n;
-  r->last_dtype = dtype;
-  r->have_backup = false;
-  if (w == 1) {  // client.py:896-900
-    int rc = pcclb_finalize(d_buf, n, dtype, op, 1, stream);
-    if (rc) return rc;
-    PCCLB_CUDA(cudaStreamSynchronize(s));
-    return PCCLB_OK;
-  }
-  Signal *me = sig_of(r->ws);
-  r->timer.n = 0;
-  PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
-  const uint64_t timeout_ns = (uint64_t)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
-  int rc;
-  if (quantize)
-    rc = quant_allreduce(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
-  else if (dtype == PCCLB_F32)
-    rc = plain_allreduce<float>(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
-  else
-    rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
-  if (rc) return rc;
-  PCCLB_CUDA(cudaMemcpyAsync(r->status_host, &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  PCCLB_CUDA(cudaStreamSynchronize(s));
-  if (out_stats) {
     out_stats->n_phases = 0;
-    for (int i = 1; i < r->timer.n && i < 16; ++i) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, r->timer.ev[i - 1], r->timer.ev[i]);
-      out_stats->phase_ms[out_stats->n_phases++] = ms;
-    }
+    if (o.timed)
+      for (int i = 1; i < r->timer.n && i < 16; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r->timer.ev[i - 1], r->timer.ev[i]);
+        out_stats->phase_ms[out_stats->n_phases++] = ms;
+      }
   }
-  const uint32_t st = *r->status_host;
+  const uint32_t st = r->status_host[ticket];
+  r->last_n = o.n;
+  r->last_dtype = o.dtype;
   // zero-copy ops never write the buffer before their last barrier, so an
   // aborted one left it untouched; staged ops restore from the copy-in
-  const bool zc = !quantize && r->last_zero_copy;
-  r->have_backup = (st == 0) || !zc;
+  r->have_backup = w > 1 && ((st == 0) || !o.zero_copy);
   if (st == 0) return PCCLB_OK;
-  if (!zc) {  // restore the caller's bytes (collective.py:568-574)
-    PCCLB_CUDA(cudaMemcpyAsync(d_buf, r->ws + kSignalBytes, n * esz, cudaMemcpyDeviceToDevice, s));
-    PCCLB_CUDA(cudaStreamSynchronize(s));
+  if (!o.zero_copy) {  // restore the caller's bytes (collective.py:568-574)
+    PCCLB_CUDA(cudaMemcpyAsync(o.buf, r->ws + kSignalBytes, o.n * esz, cudaMemcpyDeviceToDevice, o.stream));
+    PCCLB_CUDA(cudaStreamSynchronize(o.stream));
   }
   return (int)st;
+}
+
+int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op, int quantize,
+                         uint64_t attempt, int fault_at, double timeout_s, pcclb_stats *out_stats,
+                         void *stream) {
+  uint32_t t = 0;
+  int rc = pcclb_ring_enqueue(r, d_buf, n, dtype, op, quantize, attempt, fault_at, timeout_s, stream, &t);
+  if (rc) return rc;
+  return pcclb_ring_wait(r, t, out_stats);
 }
 
 int pcclb_ring_restore(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, void *stream) {
@@ -961,6 +1012,8 @@ void pcclb_ring_destroy(pcclb_ring *r) {
   if (r->ws) cudaFree(r->ws);
   if (r->host) cudaFreeHost((void *)r->host);
   if (r->status_host) cudaFreeHost(r->status_host);
+  for (int i = 0; i < kMaxOps; ++i)
+    if (r->op_events[i]) cudaEventDestroy(r->op_events[i]);
   if (r->timer.on)
     for (int i = 0; i < 16; ++i) cudaEventDestroy(r->timer.ev[i]);
   delete r;

@@ -39,6 +39,16 @@ class ReduceStats:
     phase_ms: tuple = ()  # filled when PCCLB_RING_PROFILE=1 (csrc/ring_ipc.cu PhaseTimer)
 
 
+class RingTicket:
+    """An enqueued all-reduce attempt (the AsyncHandle of client.py:102-127)."""
+
+    def __init__(self, ring: "DeviceRing", index: int, buffer: torch.Tensor):
+        self.ring = ring
+        self.index = index
+        self.buffer = buffer  # kept alive while the engine owns it
+        self.consumed = False
+
+
 def exchange_bytes(payload: bytes, group=None) -> list[bytes]:
     """all_gather of a small byte string over the process group."""
     out: list = [None] * dist.get_world_size(group)
@@ -158,8 +168,7 @@ class DeviceRing:
         self._abort[0] = 0
 
     # -- the op --
-    def run_all_reduce(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,
-                       fault_at: int = -1, stream: torch.cuda.Stream | None = None) -> ReduceStats:
+    def _validate(self, buffer: torch.Tensor, op, quantize: bool):
         op = ReduceOp.parse(op)
         if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1 or not buffer.is_contiguous():
             raise UsageError("buffer must be a one-dimensional contiguous tensor")
@@ -169,24 +178,52 @@ class DeviceRing:
             raise UsageError(f"unsupported dtype {buffer.dtype}")
         if quantize and buffer.dtype != torch.float32:
             raise UsageError("quantization requires float32 buffers")
+        return op
+
+    def all_reduce_async(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,
+                         fault_at: int = -1, stream: torch.cuda.Stream | None = None) -> "RingTicket":
+        """Enqueue one attempt on `stream` and return at once (the engine owns
+        the buffer until the ticket is awaited; client.py:802-827)."""
+        op = self._validate(buffer, op, quantize)
         n = buffer.numel()
         self.ensure_capacity(n, buffer.dtype, quantize)
         self._attempt += 1
-        stats = Stats()
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        rc = lib().pcclb_ring_allreduce(
+        t = ctypes.c_uint32()
+        rc = lib().pcclb_ring_enqueue(
             self._handle, buffer.data_ptr(), n, DTYPE_CODE[buffer.dtype], op.code, int(quantize),
-            self._attempt, fault_at, self.timeout_s, ctypes.byref(stats), s,
+            self._attempt, fault_at, self.timeout_s, s, ctypes.byref(t),
         )
+        self._raise_for(rc, "ring_enqueue")
+        return RingTicket(self, int(t.value), buffer)
+
+    def _raise_for(self, rc: int, what: str) -> None:
+        if rc == _native.PCCLB_OK:
+            return
         if rc == _native.PCCLB_EINVAL:
             raise UsageError("ring all-reduce rejected its arguments (ranks must agree on size, dtype, "
                              "op, quantization and buffer registration)")
         if rc in _STATUS_REASON:
             reason, source = _STATUS_REASON[rc]
             raise CollectiveAborted(reason, source=source)
-        check(rc, "ring_allreduce")
+        check(rc, what)
+
+    def await_reduce(self, ticket: "RingTicket") -> ReduceStats:
+        """Block until the attempt resolves; raises CollectiveAborted after the
+        buffer was restored (collective.py:568-574)."""
+        if ticket.consumed:
+            raise UsageError("ticket already awaited")
+        ticket.consumed = True
+        stats = Stats()
+        rc = lib().pcclb_ring_wait(self._handle, ticket.index, ctypes.byref(stats))
+        self._raise_for(rc, "ring_wait")
         phases = tuple(round(stats.phase_ms[i], 4) for i in range(stats.n_phases))
         return ReduceStats(stats.tx_payload_bytes, stats.rx_payload_bytes, phases)
+
+    def run_all_reduce(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,
+                       fault_at: int = -1, stream: torch.cuda.Stream | None = None) -> ReduceStats:
+        """Synchronous attempt: enqueue + await (run_all_reduce, collective.py:489)."""
+        return self.await_reduce(self.all_reduce_async(buffer, op, quantize, fault_at, stream))
 
     def restore(self, buffer: torch.Tensor) -> None:
         """Hand back the last op's input bytes (completion veto, client.py:973-983)."""

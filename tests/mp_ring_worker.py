@@ -118,6 +118,14 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                 aborted = True
             check("nonfinite: aborted", aborted)
             check("nonfinite: restored", buf.cpu().numpy().tobytes() == mine.tobytes())
+            # several attempts in flight (all_reduce_async), awaited afterwards
+            sets = [ring_inputs(world, 10_007 + 13 * i, np.dtype("float32"), 950 + i) for i in range(3)]
+            bufs = [torch.from_numpy(x[ring.position].copy()).to(dev) for x in sets]
+            tickets = [ring.all_reduce_async(b, "avg", quantize=(i == 1)) for i, b in enumerate(bufs)]
+            for i, (t, b, x) in enumerate(zip(tickets, bufs, sets)):
+                ring.await_reduce(t)
+                want = oring.ring_allreduce_chunkwise(x, oring.ReduceOp.AVG, quantize=(i == 1))
+                check(f"async in flight [{i}]", b.cpu().numpy().tobytes() == want.tobytes())
             # completion veto restore (client.py:973-983)
             inputs = ring_inputs(world, n, np.dtype("float64"), 902)
             mine = inputs[ring.position]
