@@ -331,6 +331,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    S = n * esz
     # e2e: pinned host buffer -> device, all-reduce, result -> host
     e2e = None
     if not args.no_e2e:

@@ -50,6 +50,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -229,11 +230,11 @@ __device__ __forceinline__ void cta_range_copy(const void *src, void *dst, uint6
 
 template <typename T, int OP, int VEC>
 __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
-  if (op_failed(a.mine)) return;
-  if (blockIdx.x >= a.fold_ctas) {
+  if (blockIdx.x >= a.fold_ctas) {  // the backup runs even after a failure: restores need it
     cta_range_copy(a.bak_src, a.bak_dst, a.bak_bytes, blockIdx.x - a.fold_ctas, gridDim.x - a.fold_ctas);
     return;
   }
+  if (op_failed(a.mine)) return;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)a.fold_ctas * blockDim.x;
   const uint32_t w = a.w;
@@ -523,6 +524,15 @@ unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
   return grid_for(n_vec, kIpcThreads, ctas_per_sm);
 }
 
+// plain gather engine: copy engines (default) or SM loads (PCCLB_GATHER=sm)
+bool gather_on_copy_engines() {
+  static bool ce = [] {
+    const char *e = getenv("PCCLB_GATHER");
+    return !(e && e[0] == 's');
+  }();
+  return ce;
+}
+
 // registered slot containing [p, p + bytes), or -1
 int find_reg(const pcclb_ring *r, const void *p, uint64_t bytes) {
   const char *c = static_cast<const char *>(p);
@@ -579,13 +589,14 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     f.avg = (op == PCCLB_AVG) ? w : 0;
     unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
     f.fold_ctas = grid;
-    if (zero_copy) {
-      // backup: the caller's buffer (16B-aligned run) -> in; see FoldArgs
+    if (zero_copy && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
+      // backup: the caller's buffer -> in, on one CTA per SM next to three
+      // fold CTAs (all co-resident, so the copy overlaps the NVLink-bound fold)
+      f.fold_ctas = std::min<unsigned>(grid, 3u * (unsigned)sm_count());
       f.bak_src = buf;
       f.bak_dst = r->ws + L.in;
       f.bak_bytes = n * sizeof(T);
-      if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0) grid += (unsigned)sm_count();
-      else f.fold_ctas = grid;  // unaligned: copied below instead
+      grid = f.fold_ctas + (unsigned)sm_count();
     }
     // every source and destination must share the sub-16-byte offset
     bool vec = f.dst1 == nullptr || peel16<T>(f.dst1) == peel16<T>(f.dst0);
@@ -631,7 +642,14 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     maxn = cn > maxn ? cn : maxn;
     ++jobs;
   }
-  if (jobs) {
+  if (jobs && gather_on_copy_engines()) {
+    // verbatim chunk copies ride the copy engines: measured 759 GB/s per
+    // direction with both directions busy, vs ~655 for SM loads
+    // (tools/micro/p2p_micro.cu). CE copies cannot test the op status, so an
+    // aborted op is always restored from `in` (see pcclb_ring_wait).
+    for (uint32_t j = 0; j < jobs; ++j)
+      PCCLB_CUDA(cudaMemcpyAsync(g.dst[j], g.src[j], g.n[j] * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  } else if (jobs) {
     unsigned per = ipc_grid(maxn / Pack16<T>::N + 1, 4);
     per = (per + jobs - 1) / jobs;
     if (per < 1) per = 1;
@@ -914,14 +932,13 @@ int pcclb_ring_wait(pcclb_ring *r, uint32_t ticket, pcclb_stats *out_stats) {
   const uint32_t st = r->status_host[ticket];
   r->last_n = o.n;
   r->last_dtype = o.dtype;
-  // zero-copy ops never write the buffer before their last barrier, so an
-  // aborted one left it untouched; staged ops restore from the copy-in
-  r->have_backup = w > 1 && ((st == 0) || !o.zero_copy);
+  // `in` holds the op's input in both modes (copy-in, or the backup CTAs of
+  // a zero-copy fold, which run even when the op failed)
+  r->have_backup = w > 1;
   if (st == 0) return PCCLB_OK;
-  if (!o.zero_copy) {  // restore the caller's bytes (collective.py:568-574)
-    PCCLB_CUDA(cudaMemcpyAsync(o.buf, r->ws + kSignalBytes, o.n * esz, cudaMemcpyDeviceToDevice, o.stream));
-    PCCLB_CUDA(cudaStreamSynchronize(o.stream));
-  }
+  // restore the caller's bytes (collective.py:568-574)
+  PCCLB_CUDA(cudaMemcpyAsync(o.buf, r->ws + kSignalBytes, o.n * esz, cudaMemcpyDeviceToDevice, o.stream));
+  PCCLB_CUDA(cudaStreamSynchronize(o.stream));
   return (int)st;
 }
 

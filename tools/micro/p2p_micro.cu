@@ -1,0 +1,82 @@
+// NVLink peer bandwidth on B200 pairs: pull (remote loads) vs push (remote
+// stores) vs copy engine, one and both directions, by grid size and unroll.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o p2p_micro p2p_micro.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
+
+template <int U>
+__global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t nv) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t v = tid;
+  for (; v + (U - 1) * nth < nv; v += U * nth) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = src[v + u * nth];
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[v + u * nth] = x[u];
+  }
+  for (; v < nv; v += nth) dst[v] = src[v];
+}
+
+int main() {
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (ndev < 2) { printf("need 2 GPUs\n"); return 0; }
+  const uint64_t bytes = 512ull << 20;
+  void *a[2], *b[2];
+  cudaStream_t st[2];
+  cudaEvent_t e0[2], e1[2];
+  for (int d = 0; d < 2; ++d) {
+    CK(cudaSetDevice(d));
+    CK(cudaDeviceEnablePeerAccess(1 - d, 0));
+    CK(cudaMalloc(&a[d], bytes)); CK(cudaMalloc(&b[d], bytes));
+    CK(cudaMemset(a[d], d + 1, bytes));
+    CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+    cudaEventCreate(&e0[d]); cudaEventCreate(&e1[d]);
+  }
+  const uint64_t nv = bytes / 16;
+  // mode: 0 pull (dev d reads peer's a into own b), 1 push (dev d writes own a into peer's b), 2 CE pull
+  auto run = [&](int mode, bool bidir, int grid, int unroll) -> double {
+    float best = 1e9;
+    for (int rep = 0; rep < 4; ++rep) {
+      for (int d = 0; d < (bidir ? 2 : 1); ++d) {
+        cudaSetDevice(d);
+        cudaEventRecord(e0[d], st[d]);
+        const uint4 *src = (const uint4 *)(mode == 0 || mode == 2 ? a[1 - d] : a[d]);
+        uint4 *dst = (uint4 *)(mode == 1 ? b[1 - d] : b[d]);
+        if (mode == 2) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st[d]);
+        else if (unroll == 1) copy_kernel<1><<<grid, 512, 0, st[d]>>>(src, dst, nv);
+        else if (unroll == 4) copy_kernel<4><<<grid, 512, 0, st[d]>>>(src, dst, nv);
+        else copy_kernel<8><<<grid, 512, 0, st[d]>>>(src, dst, nv);
+        cudaEventRecord(e1[d], st[d]);
+      }
+      float worst = 0;
+      for (int d = 0; d < (bidir ? 2 : 1); ++d) {
+        cudaSetDevice(d);
+        cudaEventSynchronize(e1[d]);
+        float ms; cudaEventElapsedTime(&ms, e0[d], e1[d]);
+        worst = ms > worst ? ms : worst;
+      }
+      if (rep > 0 && worst < best) best = worst;
+    }
+    return bytes / (best * 1e-3) / 1e9;
+  };
+  const char *names[3] = {"pull", "push", "CE"};
+  for (int mode = 0; mode < 3; ++mode)
+    for (int bidir = 0; bidir < 2; ++bidir) {
+      if (mode == 2) {
+        printf("%-4s %s : %7.1f GB/s per direction\n", names[mode], bidir ? "bidir" : "unidir", run(mode, bidir, 0, 0));
+        continue;
+      }
+      for (int grid : {148, 296, 592})
+        for (int u : {1, 4, 8})
+          printf("%-4s %s grid=%4d x512 U=%d : %7.1f GB/s per direction\n", names[mode], bidir ? "bidir" : "unidir", grid, u,
+                 run(mode, bidir, grid, u));
+    }
+  CK(cudaGetLastError());
+  return 0;
+}
