@@ -331,7 +331,11 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
     S = n * esz
+    algbw = S / (ms_max * 1e-3) / 1e9
+    busbw = algbw * 2 * (world - 1) / world if world > 1 else 0.0
     # e2e: pinned host buffer -> device, all-reduce, result -> host
     e2e = None
     if not args.no_e2e:

@@ -202,17 +202,25 @@ struct FoldArgs {
   uint32_t fold_ctas;
   const void *bak_src;
   void *bak_dst;
+  uint64_t bak_skip_lo, bak_skip_hi;  // byte range the fold itself backs up (own chunk)
   uint64_t bak_bytes;
+  T *bak_own;  // fold CTAs: save src[w-1] (this rank's own input) here
 };
 
-// plain 16-byte-vector copy by a subset of CTAs (both pointers 16B-aligned)
+// copy by a subset of CTAs: 16-byte vectors, with byte head/tail peeled
+// (src and dst must share their offset modulo 16)
 __device__ __forceinline__ void cta_range_copy(const void *src, void *dst, uint64_t bytes,
                                                uint32_t cta, uint32_t nctas) {
-  const uint4 *s4 = static_cast<const uint4 *>(src);
-  uint4 *d4 = static_cast<uint4 *>(dst);
-  const uint64_t nv = bytes / 16;
+  const char *sc = static_cast<const char *>(src);
+  char *dc = static_cast<char *>(dst);
   const uint64_t tid = (uint64_t)cta * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)nctas * blockDim.x;
+  uint64_t head = (16 - (reinterpret_cast<uintptr_t>(sc) & 15)) & 15;
+  if (head > bytes) head = bytes;
+  if (tid < head) dc[tid] = sc[tid];
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(sc + head);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dc + head);
+  const uint64_t nv = (bytes - head) / 16;
   uint64_t v = tid;
   for (; v + 3 * nth < nv; v += 4 * nth) {
     uint4 a = __ldcs(s4 + v), b = __ldcs(s4 + v + nth), c = __ldcs(s4 + v + 2 * nth), d = __ldcs(s4 + v + 3 * nth);
@@ -222,16 +230,17 @@ __device__ __forceinline__ void cta_range_copy(const void *src, void *dst, uint6
     __stcs(d4 + v + 3 * nth, d);
   }
   for (; v < nv; v += nth) __stcs(d4 + v, __ldcs(s4 + v));
-  const uint64_t t0 = nv * 16;
-  const char *sc = static_cast<const char *>(src);
-  char *dc = static_cast<char *>(dst);
+  const uint64_t t0 = head + nv * 16;
   if (tid < bytes - t0) dc[t0 + tid] = sc[t0 + tid];
 }
 
 template <typename T, int OP, int VEC>
 __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
   if (blockIdx.x >= a.fold_ctas) {  // the backup runs even after a failure: restores need it
-    cta_range_copy(a.bak_src, a.bak_dst, a.bak_bytes, blockIdx.x - a.fold_ctas, gridDim.x - a.fold_ctas);
+    const uint32_t c = blockIdx.x - a.fold_ctas, nc = gridDim.x - a.fold_ctas;
+    cta_range_copy(a.bak_src, a.bak_dst, a.bak_skip_lo, c, nc);
+    cta_range_copy(static_cast<const char *>(a.bak_src) + a.bak_skip_hi,
+                   static_cast<char *>(a.bak_dst) + a.bak_skip_hi, a.bak_bytes - a.bak_skip_hi, c, nc);
     return;
   }
   if (op_failed(a.mine)) return;
@@ -242,6 +251,7 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
   auto one = [&](uint64_t i) {
     T acc = a.src[0][i];
     for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.src[k][i], acc);
+    if (a.bak_own) a.bak_own[i] = a.src[w - 1][i];
     acc = fin(acc);
     a.dst0[i] = acc;
     if (a.dst1) a.dst1[i] = acc;
@@ -256,13 +266,14 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
     const uint64_t nv = (a.n - head) / N;
     for (uint64_t v = tid; v < nv; v += nth) {
       const uint64_t i = head + v * N;
-      Pack16<T> acc = ld16(a.src[0] + i);
+      Pack16<T> acc = ld16(a.src[0] + i), x;
 #pragma unroll 8
       for (uint32_t k = 1; k < w; ++k) {
-        Pack16<T> x = ld16(a.src[k] + i);
+        x = ld16(a.src[k] + i);
 #pragma unroll
         for (int e = 0; e < N; ++e) acc.e[e] = reduce_op<OP>(x.e[e], acc.e[e]);
       }
+      if (a.bak_own) st16(a.bak_own + i, x);  // x = src[w-1], this rank's input
 #pragma unroll
       for (int e = 0; e < N; ++e) acc.e[e] = fin(acc.e[e]);
       st16(a.dst0 + i, acc);
@@ -569,6 +580,8 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     desc = ((uint64_t)(slot + 1) << 40) | off;
     for (uint32_t j = 0; j < w; ++j)
       inputs[j] = reinterpret_cast<const T *>(j == rank ? (const char *)buf : r->reg[slot].peer[j] + off);
+    if (own_n == 0 || (reinterpret_cast<uintptr_t>(buf) & 15) != 0)  // rare: no fused backup
+      PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
   } else {
     // copy-in: the caller's bytes become the backup and the peers' fold input
     PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
@@ -582,7 +595,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     FoldArgs<T> f{};
     for (uint32_t k = 0; k < w; ++k) f.src[k] = inputs[(own + k) % w] + own_lo;
     f.dst0 = reinterpret_cast<T *>(r->ws + res_off(L, own_lo, sizeof(T)));
-    f.dst1 = zero_copy ? nullptr : buf + own_lo;
+    f.dst1 = buf + own_lo;  // nobody else reads this rank's own chunk
     f.mine = me;
     f.n = own_n;
     f.w = w;
@@ -591,11 +604,16 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     f.fold_ctas = grid;
     if (zero_copy && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
       // backup: the caller's buffer -> in, on one CTA per SM next to three
-      // fold CTAs (all co-resident, so the copy overlaps the NVLink-bound fold)
+      // fold CTAs (all co-resident, so the copy overlaps the NVLink-bound
+      // fold). The fold writes the own chunk in place, so it saves that
+      // chunk's input itself and the copy CTAs skip it.
       f.fold_ctas = std::min<unsigned>(grid, 3u * (unsigned)sm_count());
       f.bak_src = buf;
       f.bak_dst = r->ws + L.in;
       f.bak_bytes = n * sizeof(T);
+      f.bak_skip_lo = own_lo * sizeof(T);
+      f.bak_skip_hi = (own_lo + own_n) * sizeof(T);
+      f.bak_own = reinterpret_cast<T *>(r->ws + L.in) + own_lo;
       grid = f.fold_ctas + (unsigned)sm_count();
     }
     // every source and destination must share the sub-16-byte offset
@@ -620,8 +638,6 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
 #undef PCCLB_IPC_FOLD
     PCCLB_LAUNCH_CHECK();
   }
-  if (zero_copy && (own_n == 0 || (reinterpret_cast<uintptr_t>(buf) & 15) != 0))
-    PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
   r->timer.mark(s);
   rc = launch_barrier(r, attempt, 1, fault_at, nullptr, timeout_ns, s);
   if (rc) return rc;
@@ -631,7 +647,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   uint32_t jobs = 0;
   uint64_t maxn = 0;
   for (uint32_t c = 0; c < w; ++c) {
-    if (c == own && !zero_copy) continue;  // already written by the fold
+    if (c == own) continue;  // written by the fold
     const uint64_t cn = lo[2 * c + 1] - lo[2 * c];
     if (!cn) continue;
     const uint32_t owner = (c + w - 1) % w;
