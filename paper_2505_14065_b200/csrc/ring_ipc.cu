@@ -51,6 +51,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -234,8 +235,10 @@ __device__ __forceinline__ void cta_range_copy(const void *src, void *dst, uint6
   if (tid < bytes - t0) dc[t0 + tid] = sc[t0 + tid];
 }
 
+constexpr int kFoldThreads = 256;  // 64 regs/thread: 4 CTAs (3 fold + 1 copy) fit an SM
+
 template <typename T, int OP, int VEC>
-__global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
+__global__ void __launch_bounds__(kFoldThreads) ipc_fold_kernel(const __grid_constant__ FoldArgs<T> a) {
   if (blockIdx.x >= a.fold_ctas) {  // the backup runs even after a failure: restores need it
     const uint32_t c = blockIdx.x - a.fold_ctas, nc = gridDim.x - a.fold_ctas;
     cta_range_copy(a.bak_src, a.bak_dst, a.bak_skip_lo, c, nc);
@@ -243,10 +246,15 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
                    static_cast<char *>(a.bak_dst) + a.bak_skip_hi, a.bak_bytes - a.bak_skip_hi, c, nc);
     return;
   }
-  if (op_failed(a.mine)) return;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)a.fold_ctas * blockDim.x;
   const uint32_t w = a.w;
+  if (op_failed(a.mine)) {
+    // no fold: still back up the own chunk the copy CTAs skip
+    if (a.bak_own)
+      for (uint64_t i = tid; i < a.n; i += nth) a.bak_own[i] = a.src[w - 1][i];
+    return;
+  }
   auto fin = [&](T v) { return a.avg ? x86_div(v, (T)a.avg) : v; };
   auto one = [&](uint64_t i) {
     T acc = a.src[0][i];
@@ -264,21 +272,39 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_fold_kernel(const __grid_cons
     if (head > a.n) head = a.n;
     if (tid < head) one(tid);
     const uint64_t nv = (a.n - head) / N;
-    for (uint64_t v = tid; v < nv; v += nth) {
-      const uint64_t i = head + v * N;
-      Pack16<T> acc = ld16(a.src[0] + i), x;
-#pragma unroll 8
+    // U independent vectors per thread keep U*W loads (U*(W-1) over NVLink)
+    // in flight; U shrinks as W grows so the registers stay bounded
+    auto body = [&](auto ucount, uint64_t v0) {
+      constexpr int U = decltype(ucount)::value;
+      Pack16<T> acc[U], x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = ld16(a.src[0] + head + (v0 + u * nth) * N);
+#pragma unroll 4
       for (uint32_t k = 1; k < w; ++k) {
-        x = ld16(a.src[k] + i);
 #pragma unroll
-        for (int e = 0; e < N; ++e) acc.e[e] = reduce_op<OP>(x.e[e], acc.e[e]);
+        for (int u = 0; u < U; ++u) x[u] = ld16(a.src[k] + head + (v0 + u * nth) * N);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc[u].e[e] = reduce_op<OP>(x[u].e[e], acc[u].e[e]);
       }
-      if (a.bak_own) st16(a.bak_own + i, x);  // x = src[w-1], this rank's input
 #pragma unroll
-      for (int e = 0; e < N; ++e) acc.e[e] = fin(acc.e[e]);
-      st16(a.dst0 + i, acc);
-      if (a.dst1) st16(a.dst1 + i, acc);
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = head + (v0 + u * nth) * N;
+        if (a.bak_own) st16(a.bak_own + i, x[u]);  // x = src[w-1], this rank's input
+#pragma unroll
+        for (int e = 0; e < N; ++e) acc[u].e[e] = fin(acc[u].e[e]);
+        st16(a.dst0 + i, acc[u]);
+        if (a.dst1) st16(a.dst1 + i, acc[u]);
+      }
+    };
+    uint64_t v = tid;
+    if (w <= 2) {
+      for (; v + 3 * nth < nv; v += 4 * nth) body(std::integral_constant<int, 4>{}, v);
+    } else if (w <= 4) {
+      for (; v + nth < nv; v += 2 * nth) body(std::integral_constant<int, 2>{}, v);
     }
+    for (; v < nv; v += nth) body(std::integral_constant<int, 1>{}, v);
     const uint64_t t0 = head + nv * N;
     if (tid < a.n - t0) one(t0 + tid);
   }
@@ -536,10 +562,12 @@ unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
 }
 
 // plain gather engine: copy engines (default) or SM loads (PCCLB_GATHER=sm)
+// (SM by default: with IPC-mapped peers the copy engines measured slower,
+// 1.00 vs 0.82 ms for a 512 MiB chunk each way between two B200s)
 bool gather_on_copy_engines() {
   static bool ce = [] {
     const char *e = getenv("PCCLB_GATHER");
-    return !(e && e[0] == 's');
+    return e && e[0] == 'c';
   }();
   return ce;
 }
@@ -600,7 +628,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     f.n = own_n;
     f.w = w;
     f.avg = (op == PCCLB_AVG) ? w : 0;
-    unsigned grid = ipc_grid(own_n / Pack16<T>::N + 1);
+    unsigned grid = grid_for(own_n / Pack16<T>::N + 1, kFoldThreads, 4);
     f.fold_ctas = grid;
     if (zero_copy && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
       // backup: the caller's buffer -> in, on one CTA per SM next to three
@@ -621,9 +649,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     for (uint32_t k = 0; k < w; ++k) vec = vec && peel16<T>(f.src[k]) == peel16<T>(f.dst0);
 #define PCCLB_IPC_FOLD(OPC)                                                             \
   if (vec)                                                                              \
-    ipc_fold_kernel<T, OPC, 16 / sizeof(T)><<<grid, kIpcThreads, 0, s>>>(f);            \
+    ipc_fold_kernel<T, OPC, 16 / sizeof(T)><<<grid, kFoldThreads, 0, s>>>(f);           \
   else                                                                                  \
-    ipc_fold_kernel<T, OPC, 1><<<grid, kIpcThreads, 0, s>>>(f);
+    ipc_fold_kernel<T, OPC, 1><<<grid, kFoldThreads, 0, s>>>(f);
     switch (op) {
       case PCCLB_MAX:
         PCCLB_IPC_FOLD(PCCLB_MAX);
@@ -659,10 +687,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     ++jobs;
   }
   if (jobs && gather_on_copy_engines()) {
-    // verbatim chunk copies ride the copy engines: measured 759 GB/s per
-    // direction with both directions busy, vs ~655 for SM loads
-    // (tools/micro/p2p_micro.cu). CE copies cannot test the op status, so an
-    // aborted op is always restored from `in` (see pcclb_ring_wait).
+    // verbatim chunk copies on the copy engines (759 GB/s per direction for
+    // plain peer allocations in tools/micro/p2p_micro.cu). CE copies cannot
+    // test the op status, so an aborted op is always restored from `in`.
     for (uint32_t j = 0; j < jobs; ++j)
       PCCLB_CUDA(cudaMemcpyAsync(g.dst[j], g.src[j], g.n[j] * sizeof(T), cudaMemcpyDeviceToDevice, s));
   } else if (jobs) {
