@@ -59,64 +59,65 @@ def llama3_8b_layout() -> list[tuple[str, int]]:
 # clocks
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML during the timed
+    region (a sample at start, every `period` s, and at stop)."""
 
-    FIELDS = "index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    REASONS = {  # nvmlClocksEventReason* bits
+        "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8,
+        "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+    }
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.1):
         self.index = index
-        self.proc = None
-        self.out = ""
+        self.period = period
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.h = None
+
+    def _sample(self):
+        import pynvml
+
+        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        try:
+            bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except AttributeError:  # older bindings
+            bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((sm, bits))
 
     def start(self):
-        """Start sampling; returns once the first sample arrived (or 5 s)."""
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
-            )
-        except OSError:
-            self.proc = None
+        if os.environ.get("BENCH_NO_CLOCKS"):
             return
-        self.lines = []
-        first = threading.Event()
+        try:
+            import pynvml
 
-        def pump():
-            for line in self.proc.stdout:
-                self.lines.append(line)
-                first.set()
-            first.set()
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+        except Exception:  # noqa: BLE001
+            self.h = None
+            return
 
-        self.thread = threading.Thread(target=pump, daemon=True)
+        def loop():
+            while not self.stop_ev.wait(self.period):
+                self._sample()
+
+        self.thread = threading.Thread(target=loop, daemon=True)
         self.thread.start()
-        first.wait(5.0)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["nvml unavailable"]}
+        self.stop_ev.set()
         self.thread.join(timeout=5)
-        self.out = "".join(self.lines)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.out.strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
+        self._sample()
+        sm = sorted(x for x, _ in self.samples)
+        reasons = sorted({nm for _, b in self.samples for nm, bit in self.REASONS.items() if b & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "samples": len(sm), "reasons": reasons,
+                "source": "NVML (nvidia_ml_py), sampled during the timed region"}
 
 
 def peaks() -> dict:
