@@ -371,6 +371,43 @@ __device__ __forceinline__ void gather_copy(const T *src, T *dst, T *bak, uint64
   if (tid < n - t0) one(t0 + tid);
 }
 
+// All chunk copies interleaved in one grid: iteration v moves vector v of
+// EVERY job (a load from each owner issued before any store), so every peer
+// link is busy all the time, like the fold's access pattern. Chunk lengths
+// differ by at most one element; the shared alignment is checked on the host.
+template <typename T>
+__global__ void __launch_bounds__(kIpcThreads)
+    ipc_gather_interleaved_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs, uint64_t head) {
+  if (op_failed(a.mine)) return;
+  constexpr int N = Pack16<T>::N;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t nmin = a.n[0];
+  for (uint32_t j = 1; j < jobs; ++j) nmin = a.n[j] < nmin ? a.n[j] : nmin;
+  if (head > nmin) head = nmin;
+  const uint64_t nv = (nmin - head) / N;
+  for (uint64_t v = tid; v < nv; v += nth) {
+    Pack16<T> x[kIpcMaxWorld > 8 ? 8 : kIpcMaxWorld];
+    for (uint32_t j0 = 0; j0 < jobs; j0 += 8) {
+      const uint32_t m = jobs - j0 < 8 ? jobs - j0 : 8;
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j)
+        if (j < m) x[j] = ld16(static_cast<const T *>(a.src[j0 + j]) + head + v * N);
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j)
+        if (j < m) st16(static_cast<T *>(a.dst[j0 + j]) + head + v * N, x[j]);
+    }
+  }
+  // heads and tails (incl. the longer chunks' last element) element-wise
+  const uint64_t t0 = head + nv * N;
+  for (uint32_t j = 0; j < jobs; ++j) {
+    const T *src = static_cast<const T *>(a.src[j]);
+    T *dst = static_cast<T *>(a.dst[j]);
+    if (tid < head) dst[tid] = src[tid];
+    for (uint64_t i = t0 + tid; i < a.n[j]; i += nth) dst[i] = src[i];
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __grid_constant__ GatherArgs a) {
   if (op_failed(a.mine)) return;
@@ -572,6 +609,16 @@ bool gather_on_copy_engines() {
   return ce;
 }
 
+// plain SM gather: all chunks interleaved per thread (default) or one CTA
+// group per chunk (PCCLB_GATHER=jobs)
+bool gather_interleaved() {
+  static bool il = [] {
+    const char *e = getenv("PCCLB_GATHER");
+    return !(e && e[0] == 'j');
+  }();
+  return il;
+}
+
 // registered slot containing [p, p + bytes), or -1
 int find_reg(const pcclb_ring *r, const void *p, uint64_t bytes) {
   const char *c = static_cast<const char *>(p);
@@ -693,10 +740,21 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     for (uint32_t j = 0; j < jobs; ++j)
       PCCLB_CUDA(cudaMemcpyAsync(g.dst[j], g.src[j], g.n[j] * sizeof(T), cudaMemcpyDeviceToDevice, s));
   } else if (jobs) {
-    unsigned per = ipc_grid(maxn / Pack16<T>::N + 1, 4);
-    per = (per + jobs - 1) / jobs;
-    if (per < 1) per = 1;
-    ipc_gather_plain_kernel<T><<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
+    bool same = true;
+    const uint64_t h0 = peel16<T>(g.dst[0]);
+    for (uint32_t j = 0; j < jobs; ++j)
+      same = same && peel16<T>(g.dst[j]) == h0 && peel16<T>(g.src[j]) == h0;
+    if (same && gather_interleaved()) {
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ipc_gather_interleaved_kernel<T>, kIpcThreads, 0);
+      ipc_gather_interleaved_kernel<T><<<ipc_grid(maxn / Pack16<T>::N + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(
+          g, jobs, h0);
+    } else {
+      unsigned per = ipc_grid(maxn / Pack16<T>::N + 1, 4);
+      per = (per + jobs - 1) / jobs;
+      if (per < 1) per = 1;
+      ipc_gather_plain_kernel<T><<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
+    }
     PCCLB_LAUNCH_CHECK();
   }
   r->timer.mark(s);
