@@ -295,12 +295,16 @@ __global__ void __launch_bounds__(256)
 
 // Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default)
 // measured on B200 (config-4 layout / one 1.05 GB entry / 64 x 64 MiB):
-//   V0 13.4 ms / 84 GB/s / 4.90 TB/s    V1 22.0 ms / 47 GB/s / 2.61 TB/s
-//   V2 11.6 ms / 98 GB/s / 4.04 TB/s    V3 12.1 ms / 99 GB/s / 5.64 TB/s
-using HashV0 = HashCfg<128, 64, 3, true>;   // 2 CTAs/entry, 2-D TMA, 3 x 32 KiB stages
-using HashV1 = HashCfg<256, 16, 6, false>;  // 1 CTA/entry, 1-D bulk, 96 KiB ring
-using HashV2 = HashCfg<64, 64, 4, true>;    // 4 CTAs/entry, 2-D TMA, 64 KiB ring
-using HashV3 = HashCfg<128, 32, 6, true>;   // 2 CTAs/entry, 2-D TMA, 6 x 16 KiB stages
+//   <128,64,3>  12.1 ms /  99 GB/s / 5.64 TB/s   (2-D TMA, 2 CTAs/entry)
+//   <128,32,6>  13.4 ms /  84 GB/s / 4.90 TB/s
+//   <64,64,4>   11.6 ms /  98 GB/s / 4.04 TB/s
+//   <256,16,6>  22.0 ms /  47 GB/s / 2.61 TB/s   (1-D bulk, 1 CTA/entry)
+// ncu on <128,64,3>: 23% of warp samples wait on the stage mbarrier, i.e.
+// the large entries are short of bytes in flight -> deeper rings below.
+using HashV0 = HashCfg<128, 64, 3, true>;
+using HashV1 = HashCfg<128, 64, 6, true>;   // 192 KiB ring, 1 CTA/SM
+using HashV2 = HashCfg<64, 128, 4, true>;   // 4 CTAs/entry, 128 KiB ring
+using HashV3 = HashCfg<64, 64, 6, true>;    // 4 CTAs/entry, 96 KiB ring
 
 int hash_variant() {
   static int v = [] {
