@@ -5,6 +5,8 @@
 // 2. FNV-1a-64 chain step latency (cycles) with the split lo/hi form.
 #include <cstdio>
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
@@ -37,6 +39,36 @@ __global__ void __launch_bounds__(256) tma_stream(const uint8_t *p, uint64_t byt
     for (int i = threadIdx.x; i < STAGE / 4; i += 256) acc ^= w[i];
     __syncthreads();
     if (threadIdx.x == 0 && s + NST < nst) { mbar_expect_tx(&bars[slot], STAGE); bulk(st + slot * STAGE, base + (s + NST) * STAGE, STAGE, &bars[slot]); }
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
+// 2-D TMA: the buffer viewed as [rows x 256] u32; the CTA streams its column
+// slice [x0, x0 + BOXW) through NST stages of BOXH rows
+template <int BOXW, int BOXH, int NST>
+__global__ void __launch_bounds__(128) tma2d_stream(const __grid_constant__ CUtensorMap map, uint64_t rows_per_cta, uint32_t *sink) {
+  extern __shared__ __align__(1024) uint8_t st[];
+  __shared__ __align__(8) uint64_t bars[NST];
+  constexpr int STAGE = BOXW * BOXH * 4;
+  const int x0 = (blockIdx.x % (256 / BOXW)) * BOXW;
+  const uint64_t y0 = (blockIdx.x / (256 / BOXW)) * rows_per_cta;
+  if (threadIdx.x == 0) { for (int i = 0; i < NST; ++i) mbar_init(&bars[i], 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
+  __syncthreads();
+  const uint64_t nst = rows_per_cta / BOXH;
+  auto issue = [&](uint64_t s, int slot) {
+    mbar_expect_tx(&bars[slot], STAGE);
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(st + slot * STAGE)), "l"(&map), "r"(x0), "r"((int)(y0 + s * BOXH)), "r"(smem_u32(&bars[slot])) : "memory");
+  };
+  if (threadIdx.x == 0) for (int s = 0; s < NST && s < (int)nst; ++s) issue(s, s);
+  uint32_t acc = 0, par = 0;
+  for (uint64_t s = 0; s < nst; ++s) {
+    int slot = s % NST;
+    mbar_wait(&bars[slot], (par >> slot) & 1); par ^= 1u << slot;
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(st + slot * STAGE);
+    for (int i = threadIdx.x; i < STAGE / 4; i += 128) acc ^= w[i];
+    __syncthreads();
+    if (threadIdx.x == 0 && s + NST < nst) issue(s + NST, slot);
   }
   if (acc == 0x12345678) sink[0] = acc;
 }
@@ -120,6 +152,35 @@ int main() {
     printf("ldg U=8  ctas=%4d : %8.1f GB/s total, %7.1f GB/s per CTA\n", ctas, ctas * per / ms / 1e6, per / ms / 1e6);
     ms = time_ms([&] { ldg_stream<16><<<ctas, 256>>>((const uint4 *)buf, per / 16, sink); });
     printf("ldg U=16 ctas=%4d : %8.1f GB/s total, %7.1f GB/s per CTA\n", ctas, ctas * per / ms / 1e6, per / ms / 1e6);
+  }
+  {
+    void *fp = nullptr; cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
+    auto run2d = [&](auto kern, int boxw, int boxh, int nst, int ctas) {
+      CUtensorMap m;
+      cuuint64_t dims[2] = {256, total / 1024};
+      cuuint64_t strides[1] = {1024};
+      cuuint32_t box[2] = {(cuuint32_t)boxw, (cuuint32_t)boxh};
+      cuuint32_t es[2] = {1, 1};
+      enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      int smem = boxw * boxh * 4 * nst;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int groups = ctas / (256 / boxw); if (groups < 1) groups = 1;
+      uint64_t rows = (total / 1024 / groups) / boxh * boxh;
+      if (ctas == 1 || ctas == 2) rows = (1ull << 20) / boxh * boxh;  // 1 GiB of rounds
+      float ms = time_ms([&] { kern<<<ctas, 128, smem>>>(m, rows, sink); });
+      uint64_t bytes = (uint64_t)ctas * rows * boxw * 4;
+      printf("tma2d box=%3dx%3d nst=%d ctas=%4d : %8.1f GB/s total, %7.1f GB/s per CTA (%s)\n", boxw, boxh, nst, ctas,
+             bytes / ms / 1e6, bytes / ms / 1e6 / ctas, cudaGetErrorString(cudaGetLastError()));
+    };
+    for (int ctas : {1, 2, 4, 296}) {
+      run2d(tma2d_stream<128, 64, 3>, 128, 64, 3, ctas);
+      run2d(tma2d_stream<128, 64, 6>, 128, 64, 6, ctas);
+      run2d(tma2d_stream<256, 32, 6>, 256, 32, 6, ctas);
+      run2d(tma2d_stream<64, 128, 4>, 64, 128, 4, ctas);
+    }
   }
   uint64_t *out; long long *cyc; long long h;
   CK(cudaMalloc(&out, 8 * 1024)); CK(cudaMalloc(&cyc, 8));
