@@ -87,19 +87,51 @@ struct DequantAccF {
   float mn, scale;
   bool track;
   RangeAcc r;
+  float *__restrict__ bak = nullptr;  // optional: save acc's old value first
   __device__ __forceinline__ float step(float local, uint32_t q) {
     float v = reduce_op<OP>(local, dequant1(q, mn, scale));
     if (track) r.add(v);
     return v;
   }
-  __device__ __forceinline__ void one(uint64_t i) { acc[i] = step(acc[i], codes[i]); }
+  __device__ __forceinline__ void one(uint64_t i) {
+    const float old = acc[i];
+    if (bak) bak[i] = old;
+    acc[i] = step(old, codes[i]);
+  }
   __device__ __forceinline__ void vec(uint64_t i) {
     Pack16<float> a = ld16(acc + i);
     uint32_t q = *reinterpret_cast<const uint32_t *>(codes + i);
+    if (bak) st16(bak + i, a);
 #pragma unroll
     for (int k = 0; k < 4; ++k) a.e[k] = step(a.e[k], (q >> (8 * k)) & 0xffu);
     st16(acc + i, a);
   }
+};
+
+// range of x, saving x into bak on the way (first read of a chunk)
+struct RangeBakF {
+  const float *__restrict__ x;
+  float *__restrict__ bak;
+  RangeAcc acc;
+  __device__ __forceinline__ void one(uint64_t i) {
+    const float v = x[i];
+    bak[i] = v;
+    acc.add(v);
+  }
+  __device__ __forceinline__ void vec(uint64_t i) {
+    Pack16<float> a = ld16(x + i);
+    st16(bak + i, a);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc.add(a.e[k]);
+  }
+};
+
+// plain copy src -> dst
+struct CopyF {
+  const float *__restrict__ src;
+  float *__restrict__ dst;
+  __device__ __forceinline__ void one(uint64_t i) { dst[i] = src[i]; }
+  __device__ __forceinline__ void vec(uint64_t i) { st16(dst + i, ld16(src + i)); }
 };
 
 }  // namespace pcclb

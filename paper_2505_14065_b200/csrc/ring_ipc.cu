@@ -420,30 +420,76 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __g
     gather_copy<T, false>(src, dst, nullptr, a.n[j]);
 }
 
-__global__ void __launch_bounds__(kIpcThreads) ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a) {
+// Quantized gather: every owner's final codes dequantized (+ AVG division)
+// into this rank's buffer, all jobs interleaved per thread like the plain
+// gather (codes are 1 B/elem over NVLink). Each job has its own vector head
+// (chunk starts differ modulo 4 elements).
+__global__ void __launch_bounds__(kIpcThreads)
+    ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs) {
   if (op_failed(a.mine)) return;
-  const uint32_t j = blockIdx.y;
-  const uint64_t n = a.n[j];
-  float *dst = static_cast<float *>(a.dst[j]);
-  const uint8_t *codes = static_cast<const uint8_t *>(a.src[j]);
-  const pcclb_qmeta m = *a.meta[j];
-  DequantF f{dst, codes, m.min_val, m.scale, (float)a.avg, a.avg > 1};
-  uint64_t head = dpeel16<float>(dst);
-  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
-    ew_loop<4, 2>(n, head, f);
-  else
-    ew_loop<1, 1>(n, 0, f);
+  __shared__ float s_mn[kIpcMaxWorld], s_sc[kIpcMaxWorld];
+  __shared__ uint64_t s_head[kIpcMaxWorld];
+  for (uint32_t j = threadIdx.x; j < jobs; j += blockDim.x) {
+    const pcclb_qmeta m = *a.meta[j];  // owner's meta_final (peer memory)
+    s_mn[j] = m.min_val;
+    s_sc[j] = m.scale;
+    uint64_t h = dpeel16<float>(a.dst[j]);
+    s_head[j] = h > a.n[j] ? a.n[j] : h;
+  }
+  __syncthreads();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const float avg = (float)a.avg;
+  const bool div = a.avg > 1;
+  auto val = [&](uint32_t j, uint32_t q) {
+    float d = dequant1(q, s_mn[j], s_sc[j]);
+    return div ? x86_div(d, avg) : d;
+  };
+  uint64_t nv = ~0ull;
+  for (uint32_t j = 0; j < jobs; ++j) {
+    const uint64_t v = (a.n[j] - s_head[j]) / 4;
+    nv = v < nv ? v : nv;
+  }
+  for (uint64_t v = tid; v < nv; v += nth) {
+    for (uint32_t j0 = 0; j0 < jobs; j0 += 8) {
+      const uint32_t m = jobs - j0 < 8 ? jobs - j0 : 8;
+      uint32_t q[8];
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j)
+        if (j < m)
+          q[j] = *reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(a.src[j0 + j]) + s_head[j0 + j] + v * 4);
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j)
+        if (j < m) {
+          Pack16<float> d;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) d.e[e] = val(j0 + j, (q[j] >> (8 * e)) & 0xffu);
+          st16(static_cast<float *>(a.dst[j0 + j]) + s_head[j0 + j] + v * 4, d);
+        }
+    }
+  }
+  // heads and tails element-wise
+  for (uint32_t j = 0; j < jobs; ++j) {
+    const uint8_t *codes = static_cast<const uint8_t *>(a.src[j]);
+    float *dst = static_cast<float *>(a.dst[j]);
+    const uint64_t h = s_head[j], t0 = h + nv * 4;
+    if (tid < h) dst[tid] = val(j, codes[tid]);
+    for (uint64_t i = t0 + tid; i < a.n[j]; i += nth) dst[i] = val(j, codes[i]);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // quantized step kernels (skip after a failure)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kIpcThreads)
-    ipc_range_kernel(const float *x, uint64_t n, pcclb_range *out, const Signal *mine) {
-  if (op_failed(mine)) return;
-  RangeF f{x, RangeAcc()};
+    ipc_range_kernel(const float *x, uint64_t n, pcclb_range *out, float *bak, const Signal *mine) {
+  // runs before the first barrier: also saves this (never rx) chunk's input
+  RangeBakF f{x, bak, RangeAcc()};
   uint64_t head = dpeel16<float>(x);
-  ew_loop<4, 4>(n, head, f);
+  if (dpeel16<float>(bak) == head)
+    ew_loop<4, 4>(n, head, f);
+  else
+    ew_loop<1, 1>(n, 0, f);
   range_block_commit(f.acc, out);
 }
 
@@ -467,12 +513,21 @@ __global__ void __launch_bounds__(kIpcThreads)
 template <int OP>
 __global__ void __launch_bounds__(kIpcThreads)
     ipc_dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, const pcclb_qmeta *meta,
-                           pcclb_range *next, const Signal *mine) {
-  if (op_failed(mine)) return;
+                           pcclb_range *next, float *bak, const Signal *mine) {
+  const uint64_t head = dpeel16<float>(acc);
+  const bool vec = ((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0 && dpeel16<float>(bak) == head;
+  if (op_failed(mine)) {
+    // no accumulate, but the backup of this rx chunk must exist for the restore
+    CopyF f{acc, bak};
+    if (vec)
+      ew_loop<4, 4>(n, head, f);
+    else
+      ew_loop<1, 1>(n, 0, f);
+    return;
+  }
   const pcclb_qmeta m = *meta;  // peer memory
-  DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc()};
-  uint64_t head = dpeel16<float>(acc);
-  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
+  DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc(), bak};
+  if (vec)
     ew_loop<4, 4>(n, head, f);
   else
     ew_loop<1, 1>(n, 0, f);
@@ -771,7 +826,10 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   const uint32_t pred = (rank + w - 1) % w;
   Signal *pred_sig = sig_of(r->peer_ws[pred]);
   r->timer.mark(s);
-  PCCLB_CUDA(cudaMemcpyAsync(r->ws + L.in, buf, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  // no copy-in: every chunk's input is saved into `in` by the first kernel
+  // that reads it (range for chunk `rank`, the step's dequant-accumulate for
+  // each rx chunk), which also runs when the op already failed
+  float *bak = reinterpret_cast<float *>(r->ws + L.in);
   // range slots reset
   PCCLB_CUDA(cudaMemsetAsync(me->range, 0, sizeof(pcclb_range) * (w + 1), s));
   auto span = [&](uint32_t c, uint64_t &a, uint64_t &len) {
@@ -781,7 +839,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   uint64_t a0, n0;
   span(rank % w, a0, n0);  // step-0 tx chunk = rank (collective.py:522)
   if (n0) {
-    ipc_range_kernel<<<ipc_grid(n0 / 4 + 1), kIpcThreads, 0, s>>>(buf + a0, n0, &me->range[0], me);
+    ipc_range_kernel<<<ipc_grid(n0 / 4 + 1), kIpcThreads, 0, s>>>(buf + a0, n0, &me->range[0], bak + a0, me);
     PCCLB_LAUNCH_CHECK();
   }
   r->timer.mark(s);
@@ -806,13 +864,13 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
       const unsigned grid = ipc_grid(rn / 4 + 1);
       switch (op) {
         case PCCLB_MAX:
-          ipc_dequant_acc_kernel<PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          ipc_dequant_acc_kernel<PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
           break;
         case PCCLB_MIN:
-          ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
           break;
         default:
-          ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], me);
+          ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
           break;
       }
       PCCLB_LAUNCH_CHECK();
@@ -850,10 +908,9 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     ++jobs;
   }
   if (jobs) {
-    unsigned per = ipc_grid(maxn / 4 + 1, 4);
-    per = (per + jobs - 1) / jobs;
-    if (per < 1) per = 1;
-    ipc_gather_quant_kernel<<<dim3(per, jobs), kIpcThreads, 0, s>>>(g);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ipc_gather_quant_kernel, kIpcThreads, 0);
+    ipc_gather_quant_kernel<<<ipc_grid(maxn / 4 + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(g, jobs);
     PCCLB_LAUNCH_CHECK();
   }
   r->timer.mark(s);
