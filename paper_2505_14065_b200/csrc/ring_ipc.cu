@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __g
 // gather (codes are 1 B/elem over NVLink). Each job has its own vector head
 // (chunk starts differ modulo 4 elements).
 __global__ void __launch_bounds__(kIpcThreads)
-    ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs) {
+    ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs, int vec) {
   if (op_failed(a.mine)) return;
   __shared__ float s_mn[kIpcMaxWorld], s_sc[kIpcMaxWorld];
   __shared__ uint64_t s_head[kIpcMaxWorld];
@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(kIpcThreads)
     const uint64_t v = (a.n[j] - s_head[j]) / 4;
     nv = v < nv ? v : nv;
   }
+  if (!vec) nv = 0;  // codes and floats not co-aligned: element-wise below
   for (uint64_t v = tid; v < nv; v += nth) {
     for (uint32_t j0 = 0; j0 < jobs; j0 += 8) {
       const uint32_t m = jobs - j0 < 8 ? jobs - j0 : 8;
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(kIpcThreads)
   for (uint32_t j = 0; j < jobs; ++j) {
     const uint8_t *codes = static_cast<const uint8_t *>(a.src[j]);
     float *dst = static_cast<float *>(a.dst[j]);
-    const uint64_t h = s_head[j], t0 = h + nv * 4;
+    const uint64_t h = vec ? s_head[j] : 0, t0 = h + nv * 4;
     if (tid < h) dst[tid] = val(j, codes[tid]);
     for (uint64_t i = t0 + tid; i < a.n[j]; i += nth) dst[i] = val(j, codes[i]);
   }
@@ -910,7 +911,10 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   if (jobs) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ipc_gather_quant_kernel, kIpcThreads, 0);
-    ipc_gather_quant_kernel<<<ipc_grid(maxn / 4 + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(g, jobs);
+    int vec = 1;  // u32 code loads need codes + head 4-byte aligned for every job
+    for (uint32_t j = 0; j < jobs; ++j)
+      vec &= ((reinterpret_cast<uintptr_t>(g.src[j]) + peel16<float>(g.dst[j])) & 3) == 0;
+    ipc_gather_quant_kernel<<<ipc_grid(maxn / 4 + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(g, jobs, vec);
     PCCLB_LAUNCH_CHECK();
   }
   r->timer.mark(s);
