@@ -193,6 +193,13 @@ PCCLB_API int pcclb_ring_deregister(pcclb_ring *r, uint32_t slot);
 PCCLB_API int pcclb_ring_allreduce(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op,
                          int quantize, uint64_t attempt, int fault_at, double timeout_s,
                          pcclb_stats *out_stats, void *stream);
+/* Peer memory for shared-state resync (client.py:743-798 fetches an entry
+ * from its donor): map a peer allocation by its IPC handle (refcounted per
+ * process), and copy device/peer bytes on a stream (NVLink for peer memory). */
+PCCLB_API int pcclb_ipc_open(const void *handle64, void **ptr_out);
+PCCLB_API int pcclb_ipc_close(void *ptr);
+PCCLB_API int pcclb_copy(void *dst, const void *src, uint64_t bytes, void *stream);
+
 /* Asynchronous form (all_reduce_async / await_async_reduce, client.py:802-843):
  * enqueue returns a ticket once every kernel of the op is on `stream`; wait
  * blocks until it resolves and returns the same statuses as

@@ -109,6 +109,9 @@ SIGNATURES = {
     "pcclb_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_U64)]),
     "pcclb_ring_register": (_I, [_P, _U32, _P, _U64, _P, ctypes.POINTER(_U64)]),
     "pcclb_ring_deregister": (_I, [_P, _U32]),
+    "pcclb_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
+    "pcclb_ipc_close": (_I, [_P]),
+    "pcclb_copy": (_I, [_P, _P, _U64, _P]),
 }
 
 _lib = None

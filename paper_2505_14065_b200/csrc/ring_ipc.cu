@@ -55,6 +55,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -675,6 +676,17 @@ bool gather_interleaved() {
   return il;
 }
 
+// 16-bit digest of the op parameters in the descriptor's top bits: barrier 0
+// rejects an op whose (count, dtype, op, quantize) differ across ranks, the
+// check the reference's master does on init votes (master.py:400-434)
+uint64_t param_tag(uint64_t n, int dtype, int op, bool quant) {
+  uint64_t h = n * 0x9E3779B97F4A7C15ull ^ ((uint64_t)dtype << 8) ^ ((uint64_t)op << 16) ^ (quant ? 1ull << 24 : 0);
+  h ^= h >> 29;
+  h *= 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 32;
+  return (h & 0xffffull) << 48;
+}
+
 // registered slot containing [p, p + bytes), or -1
 int find_reg(const pcclb_ring *r, const void *p, uint64_t bytes) {
   const char *c = static_cast<const char *>(p);
@@ -698,7 +710,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const int slot = find_reg(r, buf, n * sizeof(T));
   const bool zero_copy = slot >= 0;
   r->last_zero_copy = zero_copy;
-  uint64_t desc = 0;
+  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : PCCLB_F32, op, false);
   const T *inputs[kIpcMaxWorld];  // where each ring position's input lives
   r->timer.mark(s);
   if (zero_copy) {
@@ -708,7 +720,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     // is idle while the fold waits on NVLink), keeping pcclb_ring_restore
     // (completion veto) available.
     const uint64_t off = reinterpret_cast<const char *>(buf) - r->reg[slot].local;
-    desc = ((uint64_t)(slot + 1) << 40) | off;
+    desc |= ((uint64_t)(slot + 1) << 40) | off;
     for (uint32_t j = 0; j < w; ++j)
       inputs[j] = reinterpret_cast<const T *>(j == rank ? (const char *)buf : r->reg[slot].peer[j] + off);
     if (own_n == 0 || (reinterpret_cast<uintptr_t>(buf) & 15) != 0)  // rare: no fused backup
@@ -857,7 +869,8 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
         buf + ta, tn, &me->range[step], reinterpret_cast<uint8_t *>(r->ws + codes_at(codes_off, ta)),
         &me->meta[step & 1], nullptr, 1, me);
     PCCLB_LAUNCH_CHECK();
-    rc = launch_barrier(r, attempt, step, fault_at, &me->range[step], timeout_ns, s);
+    rc = launch_barrier(r, attempt, step, fault_at, &me->range[step], timeout_ns, s,
+                        param_tag(n, PCCLB_F32, op, true), step == 0);
     if (rc) return rc;
     if (rn) {
       const uint8_t *codes = reinterpret_cast<const uint8_t *>(r->peer_ws[pred] + codes_at(codes_off, ra));
@@ -1178,6 +1191,52 @@ int pcclb_ring_register(pcclb_ring *r, uint32_t slot, const void *local_ptr, uin
 int pcclb_ring_deregister(pcclb_ring *r, uint32_t slot) {
   if (!r || slot >= (uint32_t)kMaxReg) return PCCLB_EINVAL;
   r->reg[slot] = RegSlot();  // mappings stay cached until destroy
+  return PCCLB_OK;
+}
+
+namespace {
+std::mutex g_ipc_mu;
+std::map<std::string, std::pair<char *, int>> g_ipc_open;  // handle -> (ptr, refs)
+}  // namespace
+
+int pcclb_ipc_open(const void *handle64, void **ptr_out) {
+  if (!handle64 || !ptr_out) return PCCLB_EINVAL;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  std::string key(static_cast<const char *>(handle64), 64);
+  auto it = g_ipc_open.find(key);
+  if (it != g_ipc_open.end()) {
+    it->second.second++;
+    *ptr_out = it->second.first;
+    return PCCLB_OK;
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  void *p = nullptr;
+  PCCLB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  g_ipc_open.emplace(key, std::make_pair(static_cast<char *>(p), 1));
+  *ptr_out = p;
+  return PCCLB_OK;
+}
+
+int pcclb_ipc_close(void *ptr) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (auto it = g_ipc_open.begin(); it != g_ipc_open.end(); ++it) {
+    if (it->second.first == ptr) {
+      if (--it->second.second == 0) {
+        cudaError_t e = cudaIpcCloseMemHandle(ptr);
+        g_ipc_open.erase(it);
+        if (e != cudaSuccess) return cuda_status(e);
+      }
+      return PCCLB_OK;
+    }
+  }
+  return PCCLB_EINVAL;
+}
+
+int pcclb_copy(void *dst, const void *src, uint64_t bytes, void *stream) {
+  if (bytes && (!dst || !src)) return PCCLB_EINVAL;
+  if (!bytes) return PCCLB_OK;
+  PCCLB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
   return PCCLB_OK;
 }
 

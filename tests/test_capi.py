@@ -76,7 +76,7 @@ def test_sass_is_sm100a_and_uses_bulk_copies():
     out = subprocess.run(["cuobjdump", "-lelf", _native.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
-    assert "UBLKCP" in sass
+    assert "UTMALDG" in sass  # simplehash stages via 2-D TMA tensor copies
     # -fmad=false: kernels without a division (whose correctly rounded
     # Newton sequence legitimately uses FFMA) contain no fused multiply-add
     funcs = re.split(r"\n\s*Function : ", sass)
