@@ -1,0 +1,184 @@
+"""Per-rank body of the Communicator tests (one process per GPU):
+API usage errors, concurrent tags, parameter disagreement, shared-state sync
+(config 4: one drifted peer; a newcomer), and churn (config 5: two concurrent
+quantized all-reduces, one peer dropped mid-way, retry at W-1, rejoin)."""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> None:
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ring as oring
+    from oracle import simplehash as osh
+    from paper_2505_14065_b200.collective import UsageError
+    from paper_2505_14065_b200.communicator import Communicator, SyncStatus
+    from paper_2505_14065_b200.sharedstate import DType, SharedStateEntry
+
+    dev = torch.device("cuda", rank)
+    out: dict = {"rank": rank, "checks": [], "errors": []}
+
+    def check(name, ok, detail=""):
+        out["checks"].append({"name": name, "ok": bool(ok), "detail": str(detail)[:300]})
+
+    def inputs(n, seed, w=world, scale=1.0):
+        return [np.random.default_rng(seed + p).normal(0, scale, n).astype(np.float32) for p in range(w)]
+
+    try:
+        if "api" in scenarios:
+            comm = Communicator(device=dev, pool_size=2, timeout_s=20.0)
+            check("world size", comm.get_world_size() == world)
+            # usage errors before any native call (client.py:812-824, test_bindings.py:64-80)
+            for bad, what in ((torch.zeros(4, 4, device=dev), "2-D"), (torch.zeros(8, dtype=torch.int32, device=dev), "int"),
+                              (torch.zeros(8, dtype=torch.float64, device=dev), "quant f64")):
+                try:
+                    comm.all_reduce_async(bad, 5, "sum", quantize=(what == "quant f64"))
+                    check(f"usage error {what}", False)
+                except UsageError:
+                    check(f"usage error {what}", True)
+            # two tags in flight on two slots: plain AVG (tag 0) and u8 AVG (tag 1)
+            x0, x1 = inputs(100_003, 10), inputs(77_777, 20, scale=1e-2)
+            b0 = torch.from_numpy(x0[rank].copy()).to(dev)
+            b1 = torch.from_numpy(x1[rank].copy()).to(dev)
+            h0 = comm.all_reduce_async(b0, 0, "avg")
+            h1 = comm.all_reduce_async(b1, 1, "avg", quantize=True)
+            try:
+                comm.all_reduce_async(b0, 0, "avg")
+                check("tag busy", False)
+            except UsageError:
+                check("tag busy", True)
+            r1 = comm.await_async_reduce(h1)
+            r0 = comm.await_async_reduce(h0)
+            check("tag0 completed", r0.completed, r0)
+            check("tag1 completed", r1.completed, r1)
+            check("tag0 exact", b0.cpu().numpy().tobytes() == oring.ring_allreduce_chunkwise(x0, oring.ReduceOp.AVG).tobytes())
+            check("tag1 exact", b1.cpu().numpy().tobytes() == oring.ring_allreduce_chunkwise(x1, oring.ReduceOp.AVG, True).tobytes())
+            check("traffic identity", abs(r0.tx_bytes - 2 * (world - 1) / world * 100_003 * 4) <= 0.01 * r0.tx_bytes)
+            # parameter disagreement: one rank reduces a different count -> everyone aborts, bytes intact
+            n = 5000 + (1 if rank == 0 else 0)
+            x = np.random.default_rng(rank).normal(0, 1, n).astype(np.float32)
+            b = torch.from_numpy(x.copy()).to(dev)
+            r = comm.all_reduce(b, 2, "sum")
+            check("param mismatch aborted", not r.completed, r)
+            check("param mismatch intact", b.cpu().numpy().tobytes() == x.tobytes())
+            # non-finite under quantization (client.py:871-873): aborted, intact
+            x = np.random.default_rng(rank + 9).normal(0, 1, 4096).astype(np.float32)
+            if rank == world - 1:
+                x[17] = np.nan
+            b = torch.from_numpy(x.copy()).to(dev)
+            r = comm.all_reduce(b, 3, "sum", quantize=True)
+            check("nonfinite aborted", not r.completed, r)
+            check("nonfinite intact", b.cpu().numpy().tobytes() == x.tobytes())
+            comm.close()
+
+        if "sync" in scenarios:
+            comm = Communicator(device=dev, pool_size=1, timeout_s=20.0)
+            shapes = [(1283, 64), (64, 64), (16, 64), (143, 64), (64,), (2048,)]
+
+            def state(seed):
+                g = np.random.default_rng(seed)
+                return [torch.from_numpy(g.normal(0, 1, int(np.prod(s))).astype(np.float32)).to(torch.bfloat16).to(dev)
+                        for s in shapes]
+
+            tensors = state(1234)
+            if rank == 1 % world:  # the drifted peer: one bit flipped at equal revision
+                tensors[2].view(torch.uint8)[77] ^= 1
+            entries = [SharedStateEntry(f"w{i}", DType.U8, t.view(torch.uint8), revision=7) for i, t in enumerate(tensors)]
+            res = comm.sync_shared_state(entries)
+            check("drift: updated", res.status is SyncStatus.UPDATED, res)
+            ref = [osh.simplehash_c(t.view(torch.uint8).cpu().numpy()) for t in state(1234)]
+            got = [osh.simplehash_c(e.buffer.cpu().numpy()) for e in entries]
+            check("drift: popular state everywhere", got == ref)
+            res = comm.sync_shared_state(entries)
+            check("second sync is a no-op", res.status is SyncStatus.IN_SYNC and comm.stats["sync_payload_rx"] == (entries[2].nbytes if rank == 1 % world else 0), res)
+            # newcomer at revision 0 with other contents takes everything
+            if rank == world - 1:
+                for e, t in zip(entries, state(999)):
+                    e.buffer.copy_(t.view(torch.uint8))
+                    e.revision = 0
+            res = comm.sync_shared_state(entries)
+            check("newcomer: updated", res.status is SyncStatus.UPDATED, res)
+            check("newcomer: state", [osh.simplehash_c(e.buffer.cpu().numpy()) for e in entries] == ref)
+            check("newcomer: revision", all(e.revision == 7 for e in entries))
+            comm.close()
+
+        if "churn" in scenarios and world >= 3:
+            # config 5: tags 0 and 1 (two halves of a pseudo-gradient), u8 AVG, in flight together
+            comm = Communicator(device=dev, pool_size=2, timeout_s=3.0)
+            n = 250_001
+            d0, d1 = inputs(n, 100, scale=1e-2), inputs(n, 200, scale=1e-2)
+            b0 = torch.from_numpy(d0[rank].copy()).to(dev)
+            b1 = torch.from_numpy(d1[rank].copy()).to(dev)
+            dropped = world - 1
+            h0 = comm.all_reduce_async(b0, 0, "avg", quantize=True)
+            if rank != dropped:  # the dropped peer dies before tag 1 reaches the wire
+                h1 = comm.all_reduce_async(b1, 1, "avg", quantize=True)
+            r0 = comm.await_async_reduce(h0)
+            check("churn: tag0 completed", r0.completed, r0)
+            check("churn: tag0 exact at W", b0.cpu().numpy().tobytes()
+                  == oring.ring_allreduce_chunkwise(d0, oring.ReduceOp.AVG, True).tobytes())
+            if rank != dropped:
+                r1 = comm.await_async_reduce(h1)
+                check("churn: tag1 aborted", not r1.completed, r1)
+                check("churn: tag1 restored", b1.cpu().numpy().tobytes() == d1[rank].tobytes())
+            comm.close()
+            survivors = [r for r in range(world) if r != dropped]
+            sub = dist.new_group(survivors, backend="gloo")
+            if rank != dropped:
+                # the survivors retry tag 1 at W-1 in the new (reversed) ring order
+                ring_order = list(reversed(range(len(survivors))))
+                c2 = Communicator(group=sub, device=dev, pool_size=2, ring=ring_order, timeout_s=20.0)
+                r1 = c2.all_reduce(b1, 1, "avg", quantize=True)
+                check("churn: retry completed", r1.completed, r1)
+                pos = ring_order.index(survivors.index(rank))
+                order = [d1[survivors[g]] for g in ring_order]
+                want = oring.ring_allreduce(order, oring.ReduceOp.AVG, quantize=True)[pos]
+                check("churn: retry exact at W-1", b1.cpu().numpy().tobytes() == want.tobytes())
+                c2.close()
+            dist.barrier()
+            # rejoin: the returning peer syncs the survivors' state (two buffers) and all digests agree
+            comm = Communicator(device=dev, pool_size=1, timeout_s=20.0)
+            rev = 1 if rank != dropped else 0
+            entries = [SharedStateEntry("delta0", DType.F32, b0, revision=rev), SharedStateEntry("delta1", DType.F32, b1, revision=rev)]
+            res = comm.sync_shared_state(entries)
+            check("rejoin: updated", res.status is SyncStatus.UPDATED, res)
+            hs = [None] * world
+            dist.all_gather_object(hs, [osh.simplehash_c(e.buffer.cpu().numpy()) for e in entries])
+            check("rejoin: digest parity", all(h == hs[0] for h in hs), hs)
+            comm.close()
+    except Exception:  # noqa: BLE001
+        out["errors"].append(traceback.format_exc())
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+        json.dump(out, f)
+    try:
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        pass
+
+
+def _entry(rank, world, port, outdir, scenarios):
+    run(rank, world, port, outdir, scenarios)
+
+
+if __name__ == "__main__":
+    import torch.multiprocessing as mp
+
+    world, port, outdir = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    scenarios = sys.argv[4:] or ["api", "sync", "churn"]
+    mp.spawn(_entry, args=(world, port, outdir, scenarios), nprocs=world, join=True)

@@ -118,3 +118,25 @@ def test_schedule_shapes():
     for w in (2, 3, 6):
         for pos in range(w):
             assert schedule.payload_bytes(n, w, 4, pos) == pytest.approx(2 * (w - 1) / w * n * 4, rel=0.01)
+
+
+def test_select_sync_plan_rules():
+    """master.select_sync_plan rules (master.py:909-976), test_master_units.py:59-147 shape."""
+    from paper_2505_14065_b200.communicator import SyncStrategy, select_sync_plan
+
+    E = SyncStrategy.ENFORCE_POPULAR
+    # popular hash wins at the top revision; the drifted peer fetches
+    reps = {0: (E, [("w", 7, 11, 4)]), 1: (E, [("w", 7, 22, 4)]), 2: (E, [("w", 7, 11, 4)])}
+    assert select_sync_plan(reps) == {0: [], 1: [("w", 0, 7, 11)], 2: []}
+    # a higher revision beats popularity
+    reps = {0: (E, [("w", 3, 11, 4)]), 1: (E, [("w", 9, 22, 4)]), 2: (E, [("w", 3, 11, 4)])}
+    assert select_sync_plan(reps) == {0: [("w", 1, 9, 22)], 1: [], 2: [("w", 1, 9, 22)]}
+    # tie: smallest hash, then smallest peer
+    reps = {0: (E, [("w", 1, 30, 4)]), 1: (E, [("w", 1, 20, 4)]), 2: (E, [("w", 1, 20, 4)]), 3: (E, [("w", 1, 30, 4)])}
+    assert select_sync_plan(reps)[0] == [("w", 1, 1, 20)]
+    # send-only peers donate even in the minority; receive-only never donate
+    S, R = SyncStrategy.SEND_ONLY, SyncStrategy.RECEIVE_ONLY
+    reps = {0: (S, [("w", 1, 5, 4)]), 1: (E, [("w", 1, 6, 4)]), 2: (E, [("w", 1, 6, 4)])}
+    assert select_sync_plan(reps) == {0: [], 1: [("w", 0, 1, 5)], 2: [("w", 0, 1, 5)]}
+    reps = {0: (R, [("w", 1, 5, 4)]), 1: (R, [("w", 1, 6, 4)])}
+    assert isinstance(select_sync_plan(reps), str)
