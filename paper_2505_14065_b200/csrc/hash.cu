@@ -305,6 +305,10 @@ using HashV0 = HashCfg<128, 64, 3, true>;
 using HashV1 = HashCfg<128, 64, 6, true>;   // 192 KiB ring, 1 CTA/SM
 using HashV2 = HashCfg<64, 128, 4, true>;   // 4 CTAs/entry, 128 KiB ring
 using HashV3 = HashCfg<64, 64, 6, true>;    // 4 CTAs/entry, 96 KiB ring
+// Entries that would outlast the whole batch at the shared-SM rate get SMs of
+// their own: 4 lane groups of 64 (2 warps, chain-latency-bound) and a 192 KiB
+// ring, which by itself keeps any other CTA off that SM.
+using HashBig = HashCfg<64, 128, 6, true>;
 
 int hash_variant() {
   static int v = [] {
@@ -377,6 +381,7 @@ static int prepare_hash_kernels() {
   if (!rc) rc = prepare_variant<HashV1>();
   if (!rc) rc = prepare_variant<HashV2>();
   if (!rc) rc = prepare_variant<HashV3>();
+  if (!rc) rc = prepare_variant<HashBig>();
   if (rc) return rc;
   if (dev >= 0 && dev < 64) done[dev] = true;
   return PCCLB_OK;
@@ -384,8 +389,9 @@ static int prepare_hash_kernels() {
 
 template <class C>
 static int launch_batches(const std::vector<uint32_t> &order, const void *const *h_ptrs,
-                          const uint64_t *h_nbytes, uint32_t count, uint64_t *d_out,
-                          cudaStream_t s) {
+                          const uint64_t *h_nbytes, uint64_t *d_out, cudaStream_t s) {
+  const uint32_t count = (uint32_t)order.size();
+  if (count == 0) return PCCLB_OK;
   int occ = 0;
   PCCLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, simplehash_batch_kernel<C>,
                                                            C::LANES, C::SMEM));
@@ -448,6 +454,34 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   return rc;
 }
 
+// per-device side stream + events for the big/rest split (one per host thread)
+struct Fork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static Fork &fork_for_device() {
+  static thread_local Fork forks[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Fork &f = forks[dev & 63];
+  if (!f.side) {
+    if (cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess)
+      f.side = nullptr;
+  }
+  return f;
+}
+
+// PCCLB_HASH_BIG=0 disables the big-entry split (for measurements)
+static bool big_entries_enabled() {
+  static bool on = [] {
+    const char *e = getenv("PCCLB_HASH_BIG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class C>
 static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaStream_t s) {
   CUtensorMap map;
@@ -479,16 +513,42 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
   cudaStream_t s = as_stream(stream);
-  switch (hash_variant()) {
-    case 1:
-      return launch_batches<HashV1>(order, h_ptrs, h_nbytes, count, d_out, s);
-    case 2:
-      return launch_batches<HashV2>(order, h_ptrs, h_nbytes, count, d_out, s);
-    case 3:
-      return launch_batches<HashV3>(order, h_ptrs, h_nbytes, count, d_out, s);
-    default:
-      return launch_batches<HashV0>(order, h_ptrs, h_nbytes, count, d_out, s);
+  // big entries: chain time at the shared rate (~100 GB/s) beyond the batch's
+  // HBM time (total / ~6 TB/s), i.e. more than 1/64 of the bytes
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < count; ++i) total += h_nbytes[i];
+  std::vector<uint32_t> big, rest;
+  for (uint32_t k : order) {
+    const bool is_big = big_entries_enabled() && big.size() < 16 && h_nbytes[k] >= (64ull << 20) &&
+                        h_nbytes[k] > total / 64 && count > 1;
+    (is_big ? big : rest).push_back(k);
   }
+  auto launch_rest = [&](cudaStream_t st) {
+    switch (hash_variant()) {
+      case 1:
+        return launch_batches<HashV1>(rest, h_ptrs, h_nbytes, d_out, st);
+      case 2:
+        return launch_batches<HashV2>(rest, h_ptrs, h_nbytes, d_out, st);
+      case 3:
+        return launch_batches<HashV3>(rest, h_ptrs, h_nbytes, d_out, st);
+      default:
+        return launch_batches<HashV0>(rest, h_ptrs, h_nbytes, d_out, st);
+    }
+  };
+  if (big.empty()) return launch_rest(s);
+  // the big entries start first on `s`; the rest runs beside them on a side
+  // stream forked from and joined back into `s`
+  Fork &f = fork_for_device();
+  if (!f.side) return PCCLB_ECUDA;
+  rc = launch_batches<HashBig>(big, h_ptrs, h_nbytes, d_out, s);
+  if (rc) return rc;
+  PCCLB_CUDA(cudaEventRecord(f.fork, s));
+  PCCLB_CUDA(cudaStreamWaitEvent(f.side, f.fork, 0));
+  rc = launch_rest(f.side);
+  if (rc) return rc;
+  PCCLB_CUDA(cudaEventRecord(f.join, f.side));
+  PCCLB_CUDA(cudaStreamWaitEvent(s, f.join, 0));
+  return PCCLB_OK;
 }
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {

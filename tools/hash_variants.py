@@ -39,7 +39,7 @@ views, off = [], 0
 for _, n in layout:
     views.append(state[off : off + n])
     off += n
-res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0"))}
+res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0")), "big": os.environ.get("PCCLB_HASH_BIG", "1")}
 res["config4"], digests = timeit(views)
 res["single_1GB"], _ = timeit([views[0]], 3)
 eq = state[: 64 * (32 << 20)].view(64, -1)
