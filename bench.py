@@ -356,8 +356,28 @@ def bench_allreduce(args, rank, world, local, quantize=False):
         e2e_alg = S / (e2e_ms * 1e-3) / 1e9
         e2e = {"value": round(e2e_alg * 2 * (world - 1) / world if world > 1 else e2e_alg, 2), "unit": "GB/s",
                "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3)}
-    nvl_bytes = 2 * (world - 1) / world * S  # per-GPU NVLink ingress
+    nvl_bytes = 2 * (world - 1) / world * S  # per-GPU NVLink ingress (plain)
     launches_per_op = (2 + 2 + 1) if not quantize else (1 + 3 * (world - 1) + 2 + 1)
+    if not quantize:
+        # NVLink-bound: per-GPU ingress 2(W-1)/W * S against the measured peer copy
+        roof = {"bound": "nvlink", "achieved": round(nvl_bytes / (ms_max * 1e-3) / 1e9, 1),
+                "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "frac": round(nvl_bytes / (ms_max * 1e-3) / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
+                "peak_src": "measured peer copy 770 GB/s per direction (B200_PROFILING.md); "
+                            "both-ways SM pull measured 655 (tools/micro/p2p_micro.cu)",
+                "algorithmic_bytes_per_gpu": int(nvl_bytes)}
+    else:
+        # HBM-bound: per GPU (W-1) reduce steps of 14 B/elem of a chunk
+        # (quantize 5 + dequant-accumulate 9), the owner's adoption 13 B, and the
+        # gather's (W-1) x 5 B (codes in, floats out) = (19(W-1) + 13) * n_c bytes
+        n_c = (n + world - 1) // world
+        hbm_bytes = (19 * (world - 1) + 13) * n_c
+        pk = peaks()
+        ach = hbm_bytes / (ms_max * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
+                "algorithmic_bytes_per_gpu": hbm_bytes,
+                "nvlink_bytes_per_gpu": 2 * (world - 1) * n_c}
     result = {
         "value": round(busbw, 2),
         "unit": "GB/s",
@@ -368,10 +388,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
                    "elements_per_gpu": n, "ring": list(range(world)), "algbw_GBps": round(algbw, 2),
                    "buffer": "unregistered (staged copy-in)" if args.no_register else "registered once (DeviceRing.register, zero-copy reads)",
                    "busbw_definition": "algbw*2(W-1)/W", "l2": "1 GiB inputs > 126 MB L2"},
-        "roofline": {"bound": "nvlink", "achieved": round(nvl_bytes / (ms_max * 1e-3) / 1e9, 1),
-                     "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                     "frac": round(nvl_bytes / (ms_max * 1e-3) / 1e9 / NVLINK_PEER_GBS, 4), "traffic": None,
-                     "peak_src": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)"},
+        "roofline": roof,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches_per_op * args.steps,
@@ -474,7 +491,7 @@ def reference_arm(args, workload, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "local"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
