@@ -421,6 +421,38 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __g
     gather_copy<T, false>(src, dst, nullptr, a.n[j]);
 }
 
+// Push gather (zero-copy buffers only): the owner stores its folded chunk
+// straight into every peer's registered buffer (remote stores; a third
+// barrier then tells each rank that all pushes into it landed).
+template <typename T>
+struct PushArgs {
+  const T *src;                 // own result (local)
+  T *dst[kIpcMaxWorld];         // peers' registered buffers at the owned chunk
+  uint32_t ndst;
+  uint64_t n;
+  const Signal *mine;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kIpcThreads) ipc_push_kernel(const __grid_constant__ PushArgs<T> a) {
+  if (op_failed(a.mine)) return;
+  constexpr int N = Pack16<T>::N;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t head = dpeel16<T>(a.src);
+  if (head > a.n) head = a.n;
+  const uint64_t nv = (a.n - head) / N;
+  for (uint64_t v = tid; v < nv; v += nth) {
+    const Pack16<T> x = ld16(a.src + head + v * N);
+    for (uint32_t j = 0; j < a.ndst; ++j) st16(a.dst[j] + head + v * N, x);
+  }
+  const uint64_t t0 = head + nv * N;
+  for (uint32_t j = 0; j < a.ndst; ++j) {
+    if (tid < head) a.dst[j][tid] = a.src[tid];
+    for (uint64_t i = t0 + tid; i < a.n; i += nth) a.dst[j][i] = a.src[i];
+  }
+}
+
 // Quantized gather: every owner's final codes dequantized (+ AVG division)
 // into this rank's buffer, all jobs interleaved per thread like the plain
 // gather (codes are 1 B/elem over NVLink). Each job has its own vector head
@@ -666,6 +698,29 @@ bool gather_on_copy_engines() {
   return ce;
 }
 
+// gather engine for experiments: PCCLB_GATHER = il (SM, interleaved; default)
+// | jobs (SM, one CTA group per chunk) | ce (copy engines) | push (SM remote
+// stores into registered peer buffers); PCCLB_CE_SPLIT splits CE copies
+int gather_mode() {
+  static int m = [] {
+    const char *e = getenv("PCCLB_GATHER");
+    if (!e) return 0;
+    if (e[0] == 'c') return 2;
+    if (e[0] == 'p') return 3;
+    if (e[0] == 'j') return 1;
+    return 0;
+  }();
+  return m;
+}
+int ce_split() {
+  static int k = [] {
+    const char *e = getenv("PCCLB_CE_SPLIT");
+    int v = e ? atoi(e) : 1;
+    return v < 1 ? 1 : (v > 64 ? 64 : v);
+  }();
+  return k;
+}
+
 // plain SM gather: all chunks interleaved per thread (default) or one CTA
 // group per chunk (PCCLB_GATHER=jobs)
 bool gather_interleaved() {
@@ -801,12 +856,31 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     maxn = cn > maxn ? cn : maxn;
     ++jobs;
   }
-  if (jobs && gather_on_copy_engines()) {
+  if (zero_copy && gather_mode() == 3) {
+    if (own_n) {
+      PushArgs<T> pa{};
+      pa.src = reinterpret_cast<const T *>(r->ws + res_off(L, own_lo, sizeof(T)));
+      for (uint32_t j = 0; j < w; ++j)
+        if (j != rank) pa.dst[pa.ndst++] = const_cast<T *>(inputs[j]) + own_lo;
+      pa.n = own_n;
+      pa.mine = me;
+      ipc_push_kernel<T><<<ipc_grid(own_n / Pack16<T>::N + 1, 2), kIpcThreads, 0, s>>>(pa);
+      PCCLB_LAUNCH_CHECK();
+    }
+    rc = launch_barrier(r, attempt, 2, fault_at, nullptr, timeout_ns, s);
+    if (rc) return rc;
+  } else if (jobs && (gather_on_copy_engines() || gather_mode() == 2)) {
     // verbatim chunk copies on the copy engines (759 GB/s per direction for
     // plain peer allocations in tools/micro/p2p_micro.cu). CE copies cannot
     // test the op status, so an aborted op is always restored from `in`.
-    for (uint32_t j = 0; j < jobs; ++j)
-      PCCLB_CUDA(cudaMemcpyAsync(g.dst[j], g.src[j], g.n[j] * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    const int k = ce_split();
+    for (int piece = 0; piece < k; ++piece)
+      for (uint32_t j = 0; j < jobs; ++j) {
+        const uint64_t a0 = g.n[j] * piece / k, a1 = g.n[j] * (piece + 1) / k;
+        if (a1 > a0)
+          PCCLB_CUDA(cudaMemcpyAsync(static_cast<T *>(g.dst[j]) + a0, static_cast<const T *>(g.src[j]) + a0,
+                                     (a1 - a0) * sizeof(T), cudaMemcpyDeviceToDevice, s));
+      }
   } else if (jobs) {
     bool same = true;
     const uint64_t h0 = peel16<T>(g.dst[0]);
