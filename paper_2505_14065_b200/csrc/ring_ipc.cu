@@ -429,6 +429,7 @@ struct PushArgs {
   const T *src;                 // own result (local)
   T *dst[kIpcMaxWorld];         // peers' registered buffers at the owned chunk
   uint32_t ndst;
+  uint32_t vec;  // every dst shares src's offset modulo 16
   uint64_t n;
   const Signal *mine;
 };
@@ -439,9 +440,9 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_push_kernel(const __grid_cons
   constexpr int N = Pack16<T>::N;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t head = dpeel16<T>(a.src);
+  uint64_t head = a.vec ? dpeel16<T>(a.src) : 0;
   if (head > a.n) head = a.n;
-  const uint64_t nv = (a.n - head) / N;
+  const uint64_t nv = a.vec ? (a.n - head) / N : 0;
   for (uint64_t v = tid; v < nv; v += nth) {
     const Pack16<T> x = ld16(a.src + head + v * N);
     for (uint32_t j = 0; j < a.ndst; ++j) st16(a.dst[j] + head + v * N, x);
@@ -866,6 +867,8 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
         if (j != rank) pa.dst[pa.ndst++] = const_cast<T *>(inputs[j]) + own_lo;
       pa.n = own_n;
       pa.mine = me;
+      pa.vec = 1;
+      for (uint32_t j = 0; j < pa.ndst; ++j) pa.vec &= peel16<T>(pa.dst[j]) == peel16<T>(pa.src) ? 1u : 0u;
       ipc_push_kernel<T><<<ipc_grid(own_n / Pack16<T>::N + 1, 2), kIpcThreads, 0, s>>>(pa);
       PCCLB_LAUNCH_CHECK();
     }
