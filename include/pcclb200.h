@@ -75,9 +75,11 @@ typedef struct {
   uint64_t rx_payload_bytes; /* algorithmic bytes received (collective.py:348,368) */
   /* per-phase device time in ms when the engine was created with profiling
    * on (env PCCLB_RING_PROFILE=1); n_phases = 0 otherwise. Plain ops:
-   * [copy-in, barrier0, fold, barrier1, gather]. */
+   * [copy-in, barrier0, fold, barrier1, gather(+barrier2)]; quantized ops:
+   * [range, then per step (quantize, barrier, dequant-accumulate), prologue
+   * + barrier, gather]. */
   uint32_t n_phases;
-  float phase_ms[15];
+  float phase_ms[47];
 } pcclb_stats;
 
 PCCLB_API const char *pcclb_strerror(int status);

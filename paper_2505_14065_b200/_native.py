@@ -61,7 +61,7 @@ class Stats(ctypes.Structure):
         ("tx_payload_bytes", ctypes.c_uint64),
         ("rx_payload_bytes", ctypes.c_uint64),
         ("n_phases", ctypes.c_uint32),
-        ("phase_ms", ctypes.c_float * 15),
+        ("phase_ms", ctypes.c_float * 47),
     ]
 
 

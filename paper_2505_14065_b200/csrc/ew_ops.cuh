@@ -36,7 +36,7 @@ struct QuantF {
     return do_div ? x86_div(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) {
-    uint32_t q = quant1(x[i], qp.mn, qp.scale);
+    uint32_t q = quant1_fast(x[i], qp.mn, qp.scale, qp.inv);
     codes[i] = (uint8_t)q;
     if (adopt) adopt[i] = adopt_val(q);
   }
@@ -44,7 +44,7 @@ struct QuantF {
     Pack16<float> a = ld16(x + i);
     uint32_t q[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = quant1(a.e[k], qp.mn, qp.scale);
+    for (int k = 0; k < 4; ++k) q[k] = quant1_fast(a.e[k], qp.mn, qp.scale, qp.inv);
     *reinterpret_cast<uint32_t *>(codes + i) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
     if (adopt) {
       Pack16<float> d;

@@ -130,6 +130,7 @@ __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.4028234
 struct QParams {
   float mn;
   float scale;
+  float inv;  // fl(1 / scale): fast path of quant1 (exactness-guarded)
 };
 
 // (min, scale) from a span range: scale = (max - min) / 255f, 1 when 0.
@@ -139,6 +140,7 @@ __device__ __forceinline__ QParams qparams_from_range(const pcclb_range &r) {
   if (!r.seen) {
     q.mn = 0.0f;
     q.scale = 1.0f;
+    q.inv = 1.0f;
     return q;
   }
   float mn = fkey_decode(~r.kmin_inv);
@@ -147,6 +149,7 @@ __device__ __forceinline__ QParams qparams_from_range(const pcclb_range &r) {
   if (s == 0.0f) s = 1.0f;
   q.mn = mn;
   q.scale = s;
+  q.inv = __fdiv_rn(1.0f, s);
   return q;
 }
 
@@ -157,6 +160,25 @@ __device__ __forceinline__ uint32_t quant1(float x, float mn, float scale) {
   if (is_nan(t)) return 0u;
   t = fminf(fmaxf(t, 0.0f), 255.0f);
   return (uint32_t)t;
+}
+
+// Same result without a division per element. t = d * fl(1/scale) is within
+// ~2^-22 (relative) of fl(d / scale); rint can only differ if a half-integer
+// lies that close, so t is used unless its fractional part is within 2^-20
+// (relative) of 0.5, where the exact division decides. Non-finite t (d or
+// 1/scale overflowing) also takes the exact path.
+__device__ __forceinline__ uint32_t quant1_fast(float x, float mn, float scale, float inv) {
+  const float d = x86_sub(x, mn);
+  const float t = __fmul_rn(d, inv);
+  const float fl = floorf(t);
+  const float h = __fsub_rn(t, fl);            // exact for t < 2^23
+  const float m = fabsf(__fsub_rn(h, 0.5f));   // distance to the half-integer
+  if (__builtin_expect(m > __fmul_rn(t, 1e-6f) + 1e-30f, 1)) {
+    float q = (h > 0.5f) ? __fadd_rn(fl, 1.0f) : fl;
+    q = fminf(fmaxf(q, 0.0f), 255.0f);
+    return (uint32_t)q;
+  }
+  return quant1(x, mn, scale);
 }
 
 // x = f32(q) * scale (RN) + min (RN), x86 NaN rules

@@ -574,11 +574,12 @@ __global__ void __launch_bounds__(kIpcThreads)
 using namespace pcclb;
 
 struct PhaseTimer {
+  static constexpr int kMax = 48;
   bool on = false;
   int n = 0;
-  cudaEvent_t ev[16];
+  cudaEvent_t ev[kMax];
   void mark(cudaStream_t s) {
-    if (on && n < 16) cudaEventRecord(ev[n++], s);
+    if (on && n < kMax) cudaEventRecord(ev[n++], s);
   }
 };
 
@@ -948,9 +949,11 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
         buf + ta, tn, &me->range[step], reinterpret_cast<uint8_t *>(r->ws + codes_at(codes_off, ta)),
         &me->meta[step & 1], nullptr, 1, me);
     PCCLB_LAUNCH_CHECK();
+    r->timer.mark(s);
     rc = launch_barrier(r, attempt, step, fault_at, &me->range[step], timeout_ns, s,
                         param_tag(n, PCCLB_F32, op, true), step == 0);
     if (rc) return rc;
+    r->timer.mark(s);
     if (rn) {
       const uint8_t *codes = reinterpret_cast<const uint8_t *>(r->peer_ws[pred] + codes_at(codes_off, ra));
       const pcclb_qmeta *meta = &pred_sig->meta[step & 1];
@@ -1049,7 +1052,7 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
   const char *prof = getenv("PCCLB_RING_PROFILE");
   if (prof && prof[0] == '1') {
     r->timer.on = true;
-    for (int i = 0; i < 16; ++i) cudaEventCreate(&r->timer.ev[i]);
+    for (int i = 0; i < PhaseTimer::kMax; ++i) cudaEventCreate(&r->timer.ev[i]);
   }
   r->peer_ws[rank] = r->ws;
   r->imported[rank] = true;
@@ -1177,7 +1180,7 @@ int pcclb_ring_wait(pcclb_ring *r, uint32_t ticket, pcclb_stats *out_stats) {
     out_stats->rx_payload_bytes = tx;
     out_stats->n_phases = 0;
     if (o.timed)
-      for (int i = 1; i < r->timer.n && i < 16; ++i) {
+      for (int i = 1; i < r->timer.n && i <= 47; ++i) {
         float ms = 0;
         cudaEventElapsedTime(&ms, r->timer.ev[i - 1], r->timer.ev[i]);
         out_stats->phase_ms[out_stats->n_phases++] = ms;
@@ -1332,7 +1335,7 @@ void pcclb_ring_destroy(pcclb_ring *r) {
   for (int i = 0; i < kMaxOps; ++i)
     if (r->op_events[i]) cudaEventDestroy(r->op_events[i]);
   if (r->timer.on)
-    for (int i = 0; i < 16; ++i) cudaEventDestroy(r->timer.ev[i]);
+    for (int i = 0; i < PhaseTimer::kMax; ++i) cudaEventDestroy(r->timer.ev[i]);
   delete r;
 }
 

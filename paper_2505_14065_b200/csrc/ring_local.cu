@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kLocalThreads)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   auto one = [&](uint64_t i) {
-    float d = dequant1(quant1(prev[i], qp.mn, qp.scale), qp.mn, qp.scale);
+    float d = dequant1(quant1_fast(prev[i], qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
     float v = reduce_op<OP>(cur[i], d);
     cur[i] = v;
     acc.add(v);
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kLocalThreads)
     Pack16<float> pv = ld16(prev + i), cv = ld16(cur + i);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float d = dequant1(quant1(pv.e[e], qp.mn, qp.scale), qp.mn, qp.scale);
+      float d = dequant1(quant1_fast(pv.e[e], qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
       cv.e[e] = reduce_op<OP>(cv.e[e], d);
       acc.add(cv.e[e]);
     }
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kLocalThreads)
   const QParams qp = qparams_from_range(ranges[(uint64_t)c * w + w - 1]);
   const float avg = (float)P.avg;
   auto val = [&](float x) {
-    float d = dequant1(quant1(x, qp.mn, qp.scale), qp.mn, qp.scale);
+    float d = dequant1(quant1_fast(x, qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
     return P.avg ? x86_div(d, avg) : d;
   };
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
