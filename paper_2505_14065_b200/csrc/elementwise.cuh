@@ -1,8 +1,10 @@
 // Grid-stride elementwise loop with 128-bit vector bodies.
 //
 // A functor F provides
-//   __device__ void one(uint64_t i);        // scalar element i
-//   __device__ void vec(uint64_t i);        // elements [i, i+VEC), i >= head
+//   __device__ void one(uint64_t i);             // scalar element i
+//   using In = ...;                              // loaded operands of one vector
+//   __device__ In vload(uint64_t i);             // loads for elements [i, i+VEC)
+//   __device__ void vapply(uint64_t i, const In&);  // compute + stores
 // `head` scalar elements are peeled so that vec() sees 16-byte aligned
 // addresses (the host computes it); VEC == 1 selects a scalar-only loop for
 // pointer sets whose misalignments differ.
@@ -55,12 +57,20 @@ __device__ __forceinline__ void ew_loop(uint64_t n, uint64_t head, F &f) {
     if (tid < head) f.one(tid);
     const uint64_t nv = (n - head) / VEC;
     uint64_t base = tid;
-    // full unrolled rounds: no bounds checks inside
+    // full unrolled rounds: all UNROLL vectors are loaded before any is
+    // stored, so each thread keeps UNROLL loads in flight (the compiler
+    // cannot hoist loads over stores through possibly aliasing pointers)
     for (; base + (UNROLL - 1) * nth < nv; base += UNROLL * nth) {
+      typename F::In in[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) f.vec(head + (base + u * nth) * VEC);
+      for (int u = 0; u < UNROLL; ++u) in[u] = f.vload(head + (base + u * nth) * VEC);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) f.vapply(head + (base + u * nth) * VEC, in[u]);
     }
-    for (; base < nv; base += nth) f.vec(head + base * VEC);
+    for (; base < nv; base += nth) {
+      typename F::In in = f.vload(head + base * VEC);
+      f.vapply(head + base * VEC, in);
+    }
     const uint64_t t0 = head + nv * VEC;
     if (tid < n - t0) f.one(t0 + tid);
   }

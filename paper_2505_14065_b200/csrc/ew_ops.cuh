@@ -14,8 +14,9 @@ struct RangeF {
   const float *__restrict__ x;
   RangeAcc acc;
   __device__ __forceinline__ void one(uint64_t i) { acc.add(x[i]); }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<float> a = ld16_cs(x + i);
+  using In = Pack16<float>;
+  __device__ __forceinline__ In vload(uint64_t i) { return ld16_cs(x + i); }
+  __device__ __forceinline__ void vapply(uint64_t, const In &a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc.add(a.e[k]);
   }
@@ -40,8 +41,9 @@ struct QuantF {
     codes[i] = (uint8_t)q;
     if (adopt) adopt[i] = adopt_val(q);
   }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<float> a = ld16(x + i);
+  using In = Pack16<float>;
+  __device__ __forceinline__ In vload(uint64_t i) { return ld16(x + i); }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &a) {
     uint32_t q[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) q[k] = quant1_fast(a.e[k], qp.mn, qp.scale, qp.inv);
@@ -68,8 +70,9 @@ struct DequantF {
     return do_div ? x86_div(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) { out[i] = val(codes[i]); }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    uint32_t q = *reinterpret_cast<const uint32_t *>(codes + i);
+  using In = uint32_t;
+  __device__ __forceinline__ In vload(uint64_t i) { return *reinterpret_cast<const uint32_t *>(codes + i); }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &q) {
     Pack16<float> d;
 #pragma unroll
     for (int k = 0; k < 4; ++k) d.e[k] = val((q >> (8 * k)) & 0xffu);
@@ -98,12 +101,21 @@ struct DequantAccF {
     if (bak) bak[i] = old;
     acc[i] = step(old, codes[i]);
   }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<float> a = ld16(acc + i);
-    uint32_t q = *reinterpret_cast<const uint32_t *>(codes + i);
+  struct In {
+    Pack16<float> a;
+    uint32_t q;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) {
+    In v;
+    v.a = ld16(acc + i);
+    v.q = *reinterpret_cast<const uint32_t *>(codes + i);
+    return v;
+  }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    Pack16<float> a = v.a;
     if (bak) st16(bak + i, a);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a.e[k] = step(a.e[k], (q >> (8 * k)) & 0xffu);
+    for (int k = 0; k < 4; ++k) a.e[k] = step(a.e[k], (v.q >> (8 * k)) & 0xffu);
     st16(acc + i, a);
   }
 };
@@ -118,8 +130,9 @@ struct RangeBakF {
     bak[i] = v;
     acc.add(v);
   }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<float> a = ld16(x + i);
+  using In = Pack16<float>;
+  __device__ __forceinline__ In vload(uint64_t i) { return ld16(x + i); }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &a) {
     st16(bak + i, a);
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc.add(a.e[k]);
@@ -131,7 +144,9 @@ struct CopyF {
   const float *__restrict__ src;
   float *__restrict__ dst;
   __device__ __forceinline__ void one(uint64_t i) { dst[i] = src[i]; }
-  __device__ __forceinline__ void vec(uint64_t i) { st16(dst + i, ld16(src + i)); }
+  using In = Pack16<float>;
+  __device__ __forceinline__ In vload(uint64_t i) { return ld16(src + i); }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &a) { st16(dst + i, a); }
 };
 
 }  // namespace pcclb

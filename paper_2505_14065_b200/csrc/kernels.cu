@@ -29,10 +29,19 @@ struct AccumulateF {
   T *__restrict__ acc;
   const T *__restrict__ in;
   __device__ __forceinline__ void one(uint64_t i) { acc[i] = reduce_op<OP>(acc[i], in[i]); }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<T> a = ld16(acc + i), b = ld16_cs(in + i);
+  struct In {
+    Pack16<T> a, b;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) {
+    In v;
+    v.a = ld16(acc + i);
+    v.b = ld16_cs(in + i);
+    return v;
+  }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    Pack16<T> a = v.a;
 #pragma unroll
-    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = reduce_op<OP>(a.e[k], b.e[k]);
+    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = reduce_op<OP>(a.e[k], v.b.e[k]);
     st16(acc + i, a);
   }
 };
@@ -82,8 +91,10 @@ struct DivF {
   T *__restrict__ buf;
   T w;
   __device__ __forceinline__ void one(uint64_t i) { buf[i] = x86_div(buf[i], w); }
-  __device__ __forceinline__ void vec(uint64_t i) {
-    Pack16<T> a = ld16(buf + i);
+  using In = Pack16<T>;
+  __device__ __forceinline__ In vload(uint64_t i) { return ld16(buf + i); }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    Pack16<T> a = v;
 #pragma unroll
     for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = x86_div(a.e[k], w);
     st16(buf + i, a);

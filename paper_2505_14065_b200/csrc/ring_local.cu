@@ -85,6 +85,33 @@ struct FoldAllF {
     for (int e = 0; e < N; ++e) acc.e[e] = finish(acc.e[e]);
     for (uint32_t d = 0; d < w; ++d) st16(P->b[d] + j, acc);
   }
+  // two independent vectors: both fold chains' loads are in flight together
+  __device__ __forceinline__ void vec2(uint64_t i0, uint64_t i1) {
+    constexpr int N = Pack16<T>::N;
+    const uint32_t w = P->w;
+    const uint64_t j0 = lo + i0, j1 = lo + i1;
+    uint32_t r = c;
+    Pack16<T> a0 = ld16(P->b[r] + j0), a1 = ld16(P->b[r] + j1);
+#pragma unroll 4
+    for (uint32_t k = 1; k < w; ++k) {
+      r = (r + 1 == w) ? 0 : r + 1;
+      Pack16<T> x0 = ld16(P->b[r] + j0), x1 = ld16(P->b[r] + j1);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        a0.e[e] = reduce_op<OP>(x0.e[e], a0.e[e]);
+        a1.e[e] = reduce_op<OP>(x1.e[e], a1.e[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      a0.e[e] = finish(a0.e[e]);
+      a1.e[e] = finish(a1.e[e]);
+    }
+    for (uint32_t d = 0; d < w; ++d) {
+      st16(P->b[d] + j0, a0);
+      st16(P->b[d] + j1, a1);
+    }
+  }
 };
 
 template <typename T, int OP, int VEC>
@@ -109,7 +136,9 @@ __global__ void __launch_bounds__(kLocalThreads) local_fold_all_kernel(const __g
   if (head > len) head = len;
   if (tid < head) f.one(tid);
   const uint64_t nv = (len - head) / VEC;
-  for (uint64_t v = tid; v < nv; v += nth) f.vec(head + v * VEC);
+  uint64_t v = tid;
+  for (; v + nth < nv; v += 2 * nth) f.vec2(head + v * VEC, head + (v + nth) * VEC);
+  for (; v < nv; v += nth) f.vec(head + v * VEC);
   const uint64_t t0 = head + nv * VEC;
   if (tid < len - t0) f.one(t0 + tid);
 }
@@ -167,9 +196,7 @@ __global__ void __launch_bounds__(kLocalThreads)
   uint64_t head = min((uint64_t)(((16 - (a & 15)) & 15) / 4), len);
   if (tid < head) one(tid);
   const uint64_t nv = (len - head) / 4;
-  for (uint64_t v = tid; v < nv; v += nth) {
-    const uint64_t i = head + v * 4;
-    Pack16<float> pv = ld16(prev + i), cv = ld16(cur + i);
+  auto apply = [&](uint64_t i, const Pack16<float> &pv, Pack16<float> cv) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float d = dequant1(quant1_fast(pv.e[e], qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
@@ -177,6 +204,22 @@ __global__ void __launch_bounds__(kLocalThreads)
       acc.add(cv.e[e]);
     }
     st16(cur + i, cv);
+  };
+  constexpr int U = 4;  // loads of U vectors issued before any store
+  uint64_t v = tid;
+  for (; v + (U - 1) * nth < nv; v += U * nth) {
+    Pack16<float> pv[U], cv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      pv[u] = ld16(prev + head + (v + u * nth) * 4);
+      cv[u] = ld16(cur + head + (v + u * nth) * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) apply(head + (v + u * nth) * 4, pv[u], cv[u]);
+  }
+  for (; v < nv; v += nth) {
+    const uint64_t i = head + v * 4;
+    apply(i, ld16(prev + i), ld16(cur + i));
   }
   const uint64_t t0 = head + nv * 4;
   if (tid < len - t0) one(t0 + tid);
