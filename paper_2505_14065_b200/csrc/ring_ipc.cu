@@ -456,8 +456,8 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_push_kernel(const __grid_cons
 
 // Quantized gather: every owner's final codes dequantized (+ AVG division)
 // into this rank's buffer, all jobs interleaved per thread like the plain
-// gather (codes are 1 B/elem over NVLink). Each job has its own vector head
-// (chunk starts differ modulo 4 elements).
+// gather, 16 codes (one 16-byte NVLink load) per job per iteration. Each job
+// has its own head (chunk starts differ modulo 16 elements).
 __global__ void __launch_bounds__(kIpcThreads)
     ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs, int vec) {
   if (op_failed(a.mine)) return;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kIpcThreads)
     const pcclb_qmeta m = *a.meta[j];  // owner's meta_final (peer memory)
     s_mn[j] = m.min_val;
     s_sc[j] = m.scale;
-    uint64_t h = dpeel16<float>(a.dst[j]);
+    uint64_t h = vec ? dpeel64f(static_cast<const float *>(a.dst[j])) : 0;
     s_head[j] = h > a.n[j] ? a.n[j] : h;
   }
   __syncthreads();
@@ -481,25 +481,29 @@ __global__ void __launch_bounds__(kIpcThreads)
   };
   uint64_t nv = ~0ull;
   for (uint32_t j = 0; j < jobs; ++j) {
-    const uint64_t v = (a.n[j] - s_head[j]) / 4;
+    const uint64_t v = (a.n[j] - s_head[j]) / 16;
     nv = v < nv ? v : nv;
   }
   if (!vec) nv = 0;  // codes and floats not co-aligned: element-wise below
   for (uint64_t v = tid; v < nv; v += nth) {
     for (uint32_t j0 = 0; j0 < jobs; j0 += 8) {
       const uint32_t m = jobs - j0 < 8 ? jobs - j0 : 8;
-      uint32_t q[8];
+      uint4 q[8];
 #pragma unroll
       for (uint32_t j = 0; j < 8; ++j)
         if (j < m)
-          q[j] = *reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(a.src[j0 + j]) + s_head[j0 + j] + v * 4);
+          q[j] = *reinterpret_cast<const uint4 *>(static_cast<const uint8_t *>(a.src[j0 + j]) + s_head[j0 + j] + v * 16);
 #pragma unroll
       for (uint32_t j = 0; j < 8; ++j)
         if (j < m) {
-          Pack16<float> d;
+          float *dst = static_cast<float *>(a.dst[j0 + j]) + s_head[j0 + j] + v * 16;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) d.e[e] = val(j0 + j, (q[j] >> (8 * e)) & 0xffu);
-          st16(static_cast<float *>(a.dst[j0 + j]) + s_head[j0 + j] + v * 4, d);
+          for (int g = 0; g < 4; ++g) {
+            Pack16<float> d;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d.e[e] = val(j0 + j, code_byte(q[j], 4 * g + e));
+            st16(dst + 4 * g, d);
+          }
         }
     }
   }
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(kIpcThreads)
   for (uint32_t j = 0; j < jobs; ++j) {
     const uint8_t *codes = static_cast<const uint8_t *>(a.src[j]);
     float *dst = static_cast<float *>(a.dst[j]);
-    const uint64_t h = vec ? s_head[j] : 0, t0 = h + nv * 4;
+    const uint64_t h = s_head[j], t0 = h + nv * 16;
     if (tid < h) dst[tid] = val(j, codes[tid]);
     for (uint64_t i = t0 + tid; i < a.n[j]; i += nth) dst[i] = val(j, codes[i]);
   }
@@ -537,36 +541,43 @@ __global__ void __launch_bounds__(kIpcThreads)
     meta->min_val = qp.mn;
     meta->scale = qp.scale;
   }
-  QuantF f{x, codes, adopt, qp, (float)avg, avg > 1};
-  uint64_t head = dpeel16<float>(x);
-  if (((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0)
-    ew_loop<4, 4>(n, head, f);
-  else
+  const uint64_t head = dpeel64f(x);
+  if (((reinterpret_cast<uintptr_t>(codes) + head) & 15) == 0 &&
+      (!adopt || dpeel64f(adopt) == head)) {
+    Quant16F f{x, codes, adopt, qp, (float)avg, avg > 1};
+    ew_loop<16, 2>(n, head, f);
+  } else {
+    QuantF f{x, codes, adopt, qp, (float)avg, avg > 1};
     ew_loop<1, 1>(n, 0, f);
+  }
 }
 
 template <int OP>
 __global__ void __launch_bounds__(kIpcThreads)
     ipc_dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, const pcclb_qmeta *meta,
                            pcclb_range *next, float *bak, const Signal *mine) {
-  const uint64_t head = dpeel16<float>(acc);
-  const bool vec = ((reinterpret_cast<uintptr_t>(codes) + head) & 3) == 0 && dpeel16<float>(bak) == head;
+  const uint64_t head = dpeel64f(acc);
+  const bool bak_ok = dpeel16<float>(bak) == dpeel16<float>(acc);
+  const bool vec = ((reinterpret_cast<uintptr_t>(codes) + head) & 15) == 0 && bak_ok;
   if (op_failed(mine)) {
     // no accumulate, but the backup of this rx chunk must exist for the restore
     CopyF f{acc, bak};
-    if (vec)
-      ew_loop<4, 4>(n, head, f);
+    if (bak_ok)
+      ew_loop<4, 4>(n, dpeel16<float>(acc), f);
     else
       ew_loop<1, 1>(n, 0, f);
     return;
   }
   const pcclb_qmeta m = *meta;  // peer memory
-  DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc(), bak};
-  if (vec)
-    ew_loop<4, 4>(n, head, f);
-  else
+  if (vec) {
+    DequantAcc16F<OP> f{acc, codes, m.min_val, m.scale, RangeAcc(), bak};
+    ew_loop<16, 2>(n, head, f);
+    range_block_commit(f.r, next);
+  } else {
+    DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc(), bak};
     ew_loop<1, 1>(n, 0, f);
-  range_block_commit(f.r, next);
+    range_block_commit(f.r, next);
+  }
 }
 
 }  // namespace pcclb
@@ -638,10 +649,10 @@ struct Layout {
 };
 
 // Chunk-local buffers keep the chunk's sub-16-byte alignment (floats) or
-// sub-4-byte alignment (codes), so vector bodies line up with the caller's
-// buffer at the same element offset.
+// sub-16-element alignment (codes), so 16-byte vector bodies line up with the
+// caller's buffer at the same element offset.
 uint64_t res_off(const Layout &L, uint64_t lo, size_t esz) { return L.res + (lo * esz) % 16; }
-uint64_t codes_at(uint64_t off, uint64_t lo) { return off + lo % 4; }
+uint64_t codes_at(uint64_t off, uint64_t lo) { return off + lo % 16; }
 
 Layout layout_for(uint64_t n, uint32_t w, size_t esz, bool quant) {
   Layout L{};
@@ -654,11 +665,11 @@ Layout layout_for(uint64_t n, uint32_t w, size_t esz, bool quant) {
     off = up(off + nc * esz + 16);
   } else {
     L.codes0 = off;
-    off = up(off + nc + 4);
+    off = up(off + nc + 16);
     L.codes1 = off;
-    off = up(off + nc + 4);
+    off = up(off + nc + 16);
     L.codesF = off;
-    off = up(off + nc + 4);
+    off = up(off + nc + 16);
   }
   L.end = off;
   return L;
@@ -1006,9 +1017,12 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   if (jobs) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ipc_gather_quant_kernel, kIpcThreads, 0);
-    int vec = 1;  // u32 code loads need codes + head 4-byte aligned for every job
-    for (uint32_t j = 0; j < jobs; ++j)
-      vec &= ((reinterpret_cast<uintptr_t>(g.src[j]) + peel16<float>(g.dst[j])) & 3) == 0;
+    int vec = 1;  // 16-byte code loads need codes 16-byte aligned where dst is 64-byte aligned
+    for (uint32_t j = 0; j < jobs; ++j) {
+      const uintptr_t d = reinterpret_cast<uintptr_t>(g.dst[j]);
+      const uint64_t head = ((64 - (d & 63)) & 63) / 4;
+      vec &= (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.src[j]) + head) & 15) == 0;
+    }
     ipc_gather_quant_kernel<<<ipc_grid(maxn / 4 + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(g, jobs, vec);
     PCCLB_LAUNCH_CHECK();
   }
