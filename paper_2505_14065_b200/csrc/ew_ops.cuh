@@ -34,7 +34,7 @@ struct QuantF {
   bool do_div;
   __device__ __forceinline__ float adopt_val(uint32_t q) {
     float d = dequant1(q, qp.mn, qp.scale);
-    return do_div ? x86_div(d, avg) : d;
+    return do_div ? div_world(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) {
     uint32_t q = quant1_fast(x[i], qp.mn, qp.scale, qp.inv);
@@ -67,7 +67,7 @@ struct DequantF {
   bool do_div;
   __device__ __forceinline__ float val(uint32_t q) {
     float d = dequant1(q, mn, scale);
-    return do_div ? x86_div(d, avg) : d;
+    return do_div ? div_world(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) { out[i] = val(codes[i]); }
   using In = uint32_t;
@@ -209,7 +209,7 @@ struct Dequant16F {
   bool do_div;
   __device__ __forceinline__ float val(uint32_t q) {
     float d = dequant1(q, mn, scale);
-    return do_div ? x86_div(d, avg) : d;
+    return do_div ? div_world(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) { out[i] = val(codes[i]); }
   using In = uint4;
@@ -234,7 +234,7 @@ struct Quant16F {
   bool do_div;
   __device__ __forceinline__ float adopt_val(uint32_t q) {
     float d = dequant1(q, qp.mn, qp.scale);
-    return do_div ? x86_div(d, avg) : d;
+    return do_div ? div_world(d, avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) {
     uint32_t q = quant1_fast(x[i], qp.mn, qp.scale, qp.inv);

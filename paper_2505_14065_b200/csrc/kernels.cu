@@ -90,13 +90,13 @@ template <typename T>
 struct DivF {
   T *__restrict__ buf;
   T w;
-  __device__ __forceinline__ void one(uint64_t i) { buf[i] = x86_div(buf[i], w); }
+  __device__ __forceinline__ void one(uint64_t i) { buf[i] = div_world(buf[i], w); }
   using In = Pack16<T>;
   __device__ __forceinline__ In vload(uint64_t i) { return ld16(buf + i); }
   __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
     Pack16<T> a = v;
 #pragma unroll
-    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = x86_div(a.e[k], w);
+    for (int k = 0; k < Pack16<T>::N; ++k) a.e[k] = div_world(a.e[k], w);
     st16(buf + i, a);
   }
 };

@@ -92,6 +92,21 @@ __device__ __forceinline__ T x86_div(T a, T b) {
   if (__builtin_expect(is_nan(r), 0)) r = x86_nan_result(a, b);
   return r;
 }
+// AVG finalize x / W (collective.py:482). For a power-of-two W the quotient is
+// x * 2^-k exactly (the same real value rounded once, also for subnormal
+// results), which avoids the IEEE division sequence; other W divide.
+__device__ __forceinline__ float div_world(float x, float w) {
+  const uint32_t b = __float_as_uint(w);
+  if ((b & 0x007fffffu) == 0u) return x86_mul(x, __uint_as_float((254u << 23) - b));
+  return x86_div(x, w);
+}
+__device__ __forceinline__ double div_world(double x, double w) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+  if ((b & 0x000fffffffffffffull) == 0ull)
+    return x86_mul(x, __longlong_as_double((long long)((2046ull << 52) - b)));
+  return x86_div(x, w);
+}
+
 // np.maximum / np.minimum (collective.py:69-70)
 template <typename T>
 __device__ __forceinline__ T np_maximum(T a, T b) {

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kFoldThreads) ipc_fold_kernel(const __grid_con
       for (uint64_t i = tid; i < a.n; i += nth) a.bak_own[i] = a.src[w - 1][i];
     return;
   }
-  auto fin = [&](T v) { return a.avg ? x86_div(v, (T)a.avg) : v; };
+  auto fin = [&](T v) { return a.avg ? div_world(v, (T)a.avg) : v; };
   auto one = [&](uint64_t i) {
     T acc = a.src[0][i];
     for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.src[k][i], acc);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kIpcThreads)
   const bool div = a.avg > 1;
   auto val = [&](uint32_t j, uint32_t q) {
     float d = dequant1(q, s_mn[j], s_sc[j]);
-    return div ? x86_div(d, avg) : d;
+    return div ? div_world(d, avg) : d;
   };
   uint64_t nv = ~0ull;
   for (uint32_t j = 0; j < jobs; ++j) {

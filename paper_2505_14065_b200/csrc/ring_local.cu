@@ -54,7 +54,7 @@ struct FoldAllF {
   uint32_t c;
   uint64_t lo;
   __device__ __forceinline__ T finish(T acc) const {
-    return P->avg ? x86_div(acc, (T)P->avg) : acc;
+    return P->avg ? div_world(acc, (T)P->avg) : acc;
   }
   __device__ __forceinline__ void one(uint64_t i) {
     const uint32_t w = P->w;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kLocalThreads)
   const float avg = (float)P.avg;
   auto val = [&](float x) {
     float d = dequant1(quant1_fast(x, qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
-    return P.avg ? x86_div(d, avg) : d;
+    return P.avg ? div_world(d, avg) : d;
   };
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;

@@ -15,6 +15,7 @@ from paper_2505_14065_b200.ring_ipc import DeviceRing, init_from_env  # noqa: E4
 rank, world, local = init_from_env("gloo")
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 28
 quant = len(sys.argv) > 2 and sys.argv[2] == "quant"
+op = sys.argv[3] if len(sys.argv) > 3 else "avg"
 dev = torch.device("cuda", local)
 buf = torch.randn(n, device=dev) * (1e-2 if quant else 1)
 ring = DeviceRing(device=dev, capacity_bytes=16384 + n * 4 + 4 * (n // world + 1) * 4 + (1 << 20))
@@ -22,7 +23,7 @@ if os.environ.get("REGISTER", "1") == "1":
     ring.register(buf)
 rows = []
 for i in range(8):
-    st = ring.run_all_reduce(buf, "avg", quantize=quant)
+    st = ring.run_all_reduce(buf, op, quantize=quant)
     if i >= 3:
         rows.append(st.phase_ms)
 avg = [round(sum(r[k] for r in rows) / len(rows), 4) for k in range(len(rows[0]))]
