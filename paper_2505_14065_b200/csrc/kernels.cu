@@ -47,7 +47,7 @@ struct AccumulateF {
 };
 
 template <typename T, int OP, int VEC>
-__global__ void __launch_bounds__(kThreads) accumulate_kernel(T *acc, const T *in, uint64_t n,
+__global__ void __launch_bounds__(kThreads, 4) accumulate_kernel(T *acc, const T *in, uint64_t n,
                                                                uint64_t head) {
   AccumulateF<T, OP> f{acc, in};
   ew_loop<VEC, kUnroll>(n, head, f);
@@ -102,7 +102,7 @@ struct DivF {
 };
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(kThreads) div_kernel(T *buf, uint64_t n, uint64_t head, T w) {
+__global__ void __launch_bounds__(kThreads, 4) div_kernel(T *buf, uint64_t n, uint64_t head, T w) {
   DivF<T> f{buf, w};
   ew_loop<VEC, kUnroll>(n, head, f);
 }
@@ -118,7 +118,7 @@ static int launch_div(T *buf, uint64_t n, uint32_t w, cudaStream_t s) {
 
 // K2 range
 template <int VEC>
-__global__ void __launch_bounds__(kThreads) range_kernel(const float *x, uint64_t n, uint64_t head,
+__global__ void __launch_bounds__(kThreads, 4) range_kernel(const float *x, uint64_t n, uint64_t head,
                                                           pcclb_range *out) {
   RangeF f{x, RangeAcc()};
   ew_loop<VEC, kUnroll>(n, head, f);
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreads) range_kernel(const float *x, uint64_
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     quantize_kernel(const float *x, uint64_t n, uint64_t head, const pcclb_range *range,
                     uint8_t *codes, pcclb_qmeta *meta, float *adopt, uint32_t avg_div) {
   QParams qp = qparams_from_range(*range);
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     dequantize_kernel(float *out, const uint8_t *codes, uint64_t n, uint64_t head,
                       const pcclb_qmeta *meta, uint32_t avg_div) {
   DequantF f{out, codes, meta->min_val, meta->scale, (float)avg_div, avg_div > 1};
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int OP, int VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, uint64_t head,
                        const pcclb_qmeta *meta, pcclb_range *next) {
   DequantAccF<OP> f{acc, codes, meta->min_val, meta->scale, next != nullptr, RangeAcc()};

@@ -377,7 +377,7 @@ __device__ __forceinline__ void gather_copy(const T *src, T *dst, T *bak, uint64
 // link is busy all the time, like the fold's access pattern. Chunk lengths
 // differ by at most one element; the shared alignment is checked on the host.
 template <typename T>
-__global__ void __launch_bounds__(kIpcThreads)
+__global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_gather_interleaved_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs, uint64_t head) {
   if (op_failed(a.mine)) return;
   constexpr int N = Pack16<T>::N;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kIpcThreads)
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kIpcThreads) ipc_gather_plain_kernel(const __grid_constant__ GatherArgs a) {
+__global__ void __launch_bounds__(kIpcThreads, 2) ipc_gather_plain_kernel(const __grid_constant__ GatherArgs a) {
   if (op_failed(a.mine)) return;
   const uint32_t j = blockIdx.y;
   const T *src = static_cast<const T *>(a.src[j]);
@@ -435,7 +435,7 @@ struct PushArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kIpcThreads) ipc_push_kernel(const __grid_constant__ PushArgs<T> a) {
+__global__ void __launch_bounds__(kIpcThreads, 2) ipc_push_kernel(const __grid_constant__ PushArgs<T> a) {
   if (op_failed(a.mine)) return;
   constexpr int N = Pack16<T>::N;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_push_kernel(const __grid_cons
 // into this rank's buffer, all jobs interleaved per thread like the plain
 // gather, 16 codes (one 16-byte NVLink load) per job per iteration. Each job
 // has its own head (chunk starts differ modulo 16 elements).
-__global__ void __launch_bounds__(kIpcThreads)
+__global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_gather_quant_kernel(const __grid_constant__ GatherArgs a, uint32_t jobs, int vec) {
   if (op_failed(a.mine)) return;
   __shared__ float s_mn[kIpcMaxWorld], s_sc[kIpcMaxWorld];
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(kIpcThreads)
 // ---------------------------------------------------------------------------
 // quantized step kernels (skip after a failure)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kIpcThreads)
+__global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_range_kernel(const float *x, uint64_t n, pcclb_range *out, float *bak, const Signal *mine) {
   // runs before the first barrier: also saves this (never rx) chunk's input
   RangeBakF f{x, bak, RangeAcc()};
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kIpcThreads)
   range_block_commit(f.acc, out);
 }
 
-__global__ void __launch_bounds__(kIpcThreads)
+__global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_quantize_kernel(const float *x, uint64_t n, const pcclb_range *range, uint8_t *codes,
                         pcclb_qmeta *meta, float *adopt, uint32_t avg, const Signal *mine) {
   if (op_failed(mine)) return;
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kIpcThreads)
 }
 
 template <int OP>
-__global__ void __launch_bounds__(kIpcThreads)
+__global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, const pcclb_qmeta *meta,
                            pcclb_range *next, float *bak, const Signal *mine) {
   const uint64_t head = dpeel64f(acc);

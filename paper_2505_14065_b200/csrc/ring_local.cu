@@ -115,7 +115,7 @@ struct FoldAllF {
 };
 
 template <typename T, int OP, int VEC>
-__global__ void __launch_bounds__(kLocalThreads) local_fold_all_kernel(const __grid_constant__ LocalBufs<T> P) {
+__global__ void __launch_bounds__(kLocalThreads, 4) local_fold_all_kernel(const __grid_constant__ LocalBufs<T> P) {
   const uint32_t c = blockIdx.y;
   uint64_t lo, len;
   chunk_range(P.n, P.w, c, lo, len);
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kLocalThreads) local_fold_all_kernel(const __g
 // quantized hops
 // ---------------------------------------------------------------------------
 // hop 0: range of x_c over chunk c (ranges[c*w + 0])
-__global__ void __launch_bounds__(kLocalThreads)
+__global__ void __launch_bounds__(kLocalThreads, 4)
     local_q_range0_kernel(const __grid_constant__ LocalBufs<float> P, pcclb_range *ranges) {
   const uint32_t c = blockIdx.y;
   uint64_t lo, len;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kLocalThreads)
 
 // hop k >= 1: x_{c+k} <- x_{c+k} (+) D(Q(acc_{k-1})), range -> ranges[c*w + k]
 template <int OP>
-__global__ void __launch_bounds__(kLocalThreads)
+__global__ void __launch_bounds__(kLocalThreads, 4)
     local_q_hop_kernel(const __grid_constant__ LocalBufs<float> P, pcclb_range *ranges, uint32_t k) {
   const uint32_t c = blockIdx.y;
   const uint32_t w = P.w;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kLocalThreads)
 }
 
 // owner adoption + AVG + gather: every buffer's chunk c <- D(Q(acc_{W-1})) [/W]
-__global__ void __launch_bounds__(kLocalThreads)
+__global__ void __launch_bounds__(kLocalThreads, 4)
     local_q_final_kernel(const __grid_constant__ LocalBufs<float> P, const pcclb_range *ranges) {
   const uint32_t c = blockIdx.y;
   const uint32_t w = P.w;
