@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kIpcThreads, 2)
 template <int OP>
 __global__ void __launch_bounds__(kIpcThreads, 2)
     ipc_dequant_acc_kernel(float *acc, const uint8_t *codes, uint64_t n, const pcclb_qmeta *meta,
-                           pcclb_range *next, float *bak, const Signal *mine) {
+                           pcclb_range *next, float *bak, const Signal *mine, int mode) {
   const uint64_t head = dpeel64f(acc);
   const bool bak_ok = dpeel16<float>(bak) == dpeel16<float>(acc);
   const bool vec = ((reinterpret_cast<uintptr_t>(codes) + head) & 15) == 0 && bak_ok;
@@ -569,7 +569,16 @@ __global__ void __launch_bounds__(kIpcThreads, 2)
     return;
   }
   const pcclb_qmeta m = *meta;  // peer memory
-  if (vec) {
+  const uint64_t head4 = dpeel16<float>(acc);
+  if (mode == 1 && bak_ok && ((reinterpret_cast<uintptr_t>(codes) + head4) & 3) == 0) {
+    DequantAccF<OP> f{acc, codes, m.min_val, m.scale, true, RangeAcc(), bak};
+    ew_loop<4, 4>(n, head4, f);
+    range_block_commit(f.r, next);
+  } else if (vec && mode == 2) {
+    DequantAcc16F<OP> f{acc, codes, m.min_val, m.scale, RangeAcc(), bak};
+    ew_loop<16, 4>(n, head, f);
+    range_block_commit(f.r, next);
+  } else if (vec) {
     DequantAcc16F<OP> f{acc, codes, m.min_val, m.scale, RangeAcc(), bak};
     ew_loop<16, 2>(n, head, f);
     range_block_commit(f.r, next);
@@ -698,6 +707,16 @@ int launch_barrier(pcclb_ring *r, uint64_t attempt, uint32_t index, int fault_at
 
 unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
   return grid_for(n_vec, kIpcThreads, ctas_per_sm);
+}
+
+// dequant-accumulate shape (experiments): PCCLB_DQA=0 16 floats x 2 (default),
+// 1: 4 floats x 4, 2: 16 floats x 4
+int dqa_mode_value() {
+  static int m = [] {
+    const char *e = getenv("PCCLB_DQA");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
 }
 
 // plain gather engine: copy engines (default) or SM loads (PCCLB_GATHER=sm)
@@ -971,13 +990,13 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
       const unsigned grid = ipc_grid(rn / 4 + 1);
       switch (op) {
         case PCCLB_MAX:
-          ipc_dequant_acc_kernel<PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
+          ipc_dequant_acc_kernel<PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());
           break;
         case PCCLB_MIN:
-          ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
+          ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());
           break;
         default:
-          ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me);
+          ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());
           break;
       }
       PCCLB_LAUNCH_CHECK();
