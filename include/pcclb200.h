@@ -123,6 +123,17 @@ PCCLB_API int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint
                                 const pcclb_qmeta *d_meta, int op, pcclb_range *d_next_range,
                                 void *stream);
 
+/* Outer-optimizer steps of the DiLoCo loops around the all-reduce, with the
+ * reference's rounding sequence (algos.py:79-105, :236-239):
+ * delta = global - local; PlainSGD params -= lr * grad;
+ * NesterovOuter v = v*mu; v = v + delta; params -= lr * (delta + mu*v). */
+PCCLB_API int pcclb_pseudo_gradient_f32(float *delta, const float *global, const float *local,
+                                        uint64_t n, void *stream);
+PCCLB_API int pcclb_outer_sgd_f32(float *params, const float *grad, uint64_t n, float lr,
+                                  void *stream);
+PCCLB_API int pcclb_outer_nesterov_f32(float *params, const float *delta, float *velocity,
+                                       uint64_t n, float lr, float momentum, void *stream);
+
 /* sharedstate.py:87-105 simplehash over one device buffer; result to d_out[0] */
 PCCLB_API int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream);
 

@@ -88,6 +88,9 @@ SIGNATURES = {
     "pcclb_simplehash_init": (_I, [_P, _P]),
     "pcclb_simplehash_update": (_I, [_P, _P, _U64, _P]),
     "pcclb_simplehash_final": (_I, [_P, _U64, _P, _P]),
+    "pcclb_pseudo_gradient_f32": (_I, [_P, _P, _P, _U64, _P]),
+    "pcclb_outer_sgd_f32": (_I, [_P, _P, _U64, ctypes.c_float, _P]),
+    "pcclb_outer_nesterov_f32": (_I, [_P, _P, _P, _U64, ctypes.c_float, ctypes.c_float, _P]),
     "pcclb_local_scratch_bytes": (_U64, [_U32]),
     "pcclb_local_allreduce": (_I, [ctypes.POINTER(_P), _U32, _U64, _I, _I, _I, _P, _P, _P]),
     "pcclb_ring_create": (_I, [_I, _U32, _U32, _U64, ctypes.POINTER(_P)]),

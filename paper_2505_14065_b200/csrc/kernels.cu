@@ -263,3 +263,122 @@ int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint64_t n,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Outer-optimizer steps around the all-reduce, with the
+// reference's NumPy rounding sequence (algos.py:79-105, :236-239):
+//   pseudo-gradient   delta = global - local
+//   PlainSGD          params -= lr * grad                    (2 roundings)
+//   NesterovOuter     v = v * mu; v = v + delta;
+//                     params -= lr * (delta + mu * v)        (6 roundings, no FMA)
+// ---------------------------------------------------------------------------
+namespace pcclb {
+
+struct SubF {  // out = a - b
+  float *__restrict__ out;
+  const float *__restrict__ a;
+  const float *__restrict__ b;
+  __device__ __forceinline__ void one(uint64_t i) { out[i] = x86_sub(a[i], b[i]); }
+  struct In {
+    Pack16<float> x, y;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) { return In{ld16(a + i), ld16(b + i)}; }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    Pack16<float> r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r.e[k] = x86_sub(v.x.e[k], v.y.e[k]);
+    st16(out + i, r);
+  }
+};
+
+struct SgdF {  // p -= lr * g
+  float *__restrict__ p;
+  const float *__restrict__ g;
+  float lr;
+  __device__ __forceinline__ float upd(float pv, float gv) const { return x86_sub(pv, x86_mul(lr, gv)); }
+  __device__ __forceinline__ void one(uint64_t i) { p[i] = upd(p[i], g[i]); }
+  struct In {
+    Pack16<float> p, g;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) { return In{ld16(p + i), ld16(g + i)}; }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    Pack16<float> r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r.e[k] = upd(v.p.e[k], v.g.e[k]);
+    st16(p + i, r);
+  }
+};
+
+struct NesterovF {
+  float *__restrict__ p;
+  const float *__restrict__ d;
+  float *__restrict__ vel;
+  float lr, mu;
+  __device__ __forceinline__ void upd(float &pv, float dv, float &vv) const {
+    vv = x86_mul(vv, mu);
+    vv = x86_add(vv, dv);
+    pv = x86_sub(pv, x86_mul(lr, x86_add(dv, x86_mul(mu, vv))));
+  }
+  __device__ __forceinline__ void one(uint64_t i) {
+    float pv = p[i], vv = vel[i];
+    upd(pv, d[i], vv);
+    p[i] = pv;
+    vel[i] = vv;
+  }
+  struct In {
+    Pack16<float> p, d, v;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) { return In{ld16(p + i), ld16(d + i), ld16(vel + i)}; }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &in) {
+    Pack16<float> pv = in.p, vv = in.v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) upd(pv.e[k], in.d.e[k], vv.e[k]);
+    st16(p + i, pv);
+    st16(vel + i, vv);
+  }
+};
+
+template <typename F, int VEC>
+__global__ void __launch_bounds__(kThreads, 4) functor_kernel(F f, uint64_t n, uint64_t head) {
+  ew_loop<VEC, kUnroll>(n, head, f);
+}
+
+template <typename F>
+static int launch_functor(F f, uint64_t n, bool vec, uint64_t head, cudaStream_t s) {
+  if (n == 0) return PCCLB_OK;
+  unsigned grid = grid_for(n, (uint64_t)kThreads * kUnroll * 4);
+  if (vec)
+    functor_kernel<F, 4><<<grid, kThreads, 0, s>>>(f, n, head);
+  else
+    functor_kernel<F, 1><<<grid, kThreads, 0, s>>>(f, n, 0);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
+}  // namespace pcclb
+
+extern "C" {
+
+int pcclb_pseudo_gradient_f32(float *delta, const float *global, const float *local, uint64_t n,
+                              void *stream) {
+  if (n && (!delta || !global || !local)) return PCCLB_EINVAL;
+  const uint64_t h = peel16<float>(delta);
+  const bool vec = peel16<float>(global) == h && peel16<float>(local) == h;
+  return launch_functor(SubF{delta, global, local}, n, vec, h, as_stream(stream));
+}
+
+int pcclb_outer_sgd_f32(float *params, const float *grad, uint64_t n, float lr, void *stream) {
+  if (n && (!params || !grad)) return PCCLB_EINVAL;
+  const uint64_t h = peel16<float>(params);
+  return launch_functor(SgdF{params, grad, lr}, n, peel16<float>(grad) == h, h, as_stream(stream));
+}
+
+int pcclb_outer_nesterov_f32(float *params, const float *delta, float *velocity, uint64_t n, float lr,
+                             float momentum, void *stream) {
+  if (n && (!params || !delta || !velocity)) return PCCLB_EINVAL;
+  const uint64_t h = peel16<float>(params);
+  const bool vec = peel16<float>(delta) == h && peel16<float>(velocity) == h;
+  return launch_functor(NesterovF{params, delta, velocity, lr, momentum}, n, vec, h, as_stream(stream));
+}
+
+}  // extern "C"

@@ -108,3 +108,21 @@ def test_appendix_c_goldens(golden):
     for quant, key in ((False, "plain"), (True, "quant")):
         out = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.AVG, quantize=quant)
         assert osh.simplehash_c(out) == want[key]
+
+
+def test_outer_oracle_matches_reference_expressions():
+    """oracle/outer.py is the reference's own NumPy sequence (algos.py:93-100);
+    check it against a literal transcription on random data."""
+    from oracle import outer as oouter
+
+    rng = np.random.default_rng(1)
+    p = rng.normal(0, 1, 1001).astype(np.float32)
+    d = rng.normal(0, 1, 1001).astype(np.float32)
+    v = rng.normal(0, 1, 1001).astype(np.float32)
+    p2, v2 = p.copy(), v.copy()
+    oouter.nesterov_step(p, d, v, 0.5, 0.9)
+    lr, mu = np.float32(0.5), np.float32(0.9)
+    v2 = v2 * mu
+    v2 = v2 + d
+    p2 = p2 - lr * (d + mu * v2)
+    assert p.tobytes() == p2.tobytes() and v.tobytes() == v2.tobytes()
