@@ -159,6 +159,28 @@ def make_appendix_c():
     return res
 
 
+def make_outer():
+    """Run the reference's own outer optimizers (algos.py:75-105) on seeded
+    data: 4 outer steps of pseudo-gradient + Nesterov, each followed by one
+    PlainSGD step."""
+    from churncomm.algos import NesterovOuter, PlainSGD
+
+    out = {}
+    for n in (7, 4099):
+        rng = np.random.default_rng(n)
+        g = rng.normal(0, 1, n).astype(np.float32)
+        opt = NesterovOuter(n, lr=0.7, momentum=0.9)
+        sgd = PlainSGD(2.0**-6)
+        for step in range(4):
+            local = g - rng.normal(0, 1e-2, n).astype(np.float32) * np.float32(step + 1)
+            delta = g - local  # algos.py:236
+            opt.step(g, delta)
+            grad = rng.normal(0, 1, n).astype(np.float32)
+            sgd.step(g, grad)
+        out[str(n)] = {"params": simplehash(g), "velocity": simplehash(opt.velocity)}
+    return out
+
+
 def main():
     fixtures = {}
     fixtures["bounds"] = {
@@ -175,6 +197,7 @@ def main():
     fixtures["ring"] = ring
     fixtures["ring_engine_checked"] = engine_checked
     fixtures["appendix_c_w8_avg_16M"] = make_appendix_c()
+    fixtures["outer"] = make_outer()
     fixtures["generator"] = {
         "reference": "/root/reference/pkg (churncomm, pure Python/NumPy)",
         "numpy": np.__version__,

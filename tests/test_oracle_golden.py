@@ -126,3 +126,26 @@ def test_outer_oracle_matches_reference_expressions():
     v2 = v2 + d
     p2 = p2 - lr * (d + mu * v2)
     assert p.tobytes() == p2.tobytes() and v.tobytes() == v2.tobytes()
+
+
+def _outer_replay(n, oouter):
+    rng = np.random.default_rng(n)
+    g = rng.normal(0, 1, n).astype(np.float32)
+    vel = np.zeros(n, np.float32)
+    for step in range(4):
+        local = g - rng.normal(0, 1e-2, n).astype(np.float32) * np.float32(step + 1)
+        d = oouter.pseudo_gradient(g, local)
+        oouter.nesterov_step(g, d, vel, 0.7, 0.9)
+        grad = rng.normal(0, 1, n).astype(np.float32)
+        oouter.sgd_step(g, grad, 2.0**-6)
+    return g, vel
+
+
+def test_outer_oracle_matches_reference_run(golden):
+    """oracle/outer.py reproduces churncomm.algos' optimizers (golden.json 'outer')."""
+    from oracle import outer as oouter
+
+    for n, want in golden["outer"].items():
+        g, vel = _outer_replay(int(n), oouter)
+        assert osh.simplehash_c(g) == want["params"]
+        assert osh.simplehash_c(vel) == want["velocity"]
