@@ -128,3 +128,22 @@ def edge_pairs(dt) -> tuple[np.ndarray, np.ndarray]:
     ra = rng.normal(0, 1, 1001).astype(dt)
     rb = rng.normal(0, 1, 1001).astype(dt)
     return np.concatenate([a, ra]), np.concatenate([b, rb])
+
+
+# Reference wire transcripts (tests/golden/make_wire_golden.py):
+# (world, n, op, quantize, dtype, seed, chunk_bytes)
+WIRE_CASES = [
+    (2, 1000, "sum", False, "float32", 11, 256),
+    (3, 1000, "avg", False, "float32", 12, 256),
+    (3, 1001, "max", False, "float64", 13, 512),
+    (4, 999, "min", False, "float32", 14, 1024),
+    (3, 2, "sum", False, "float32", 15, 256),
+    (1, 100, "avg", False, "float32", 23, 256),
+    (2, 1000, "avg", True, "float32", 16, 256),
+    (3, 1000, "sum", True, "float32", 17, 300),
+    (4, 1003, "max", True, "float32", 18, 256),
+    (3, 2, "avg", True, "float32", 19, 256),
+    (3, 997, "min", True, "float32", 100019, 128),
+    (5, 5000, "avg", True, "float32", 20, 1024),
+    (5, 5000, "avg", False, "float64", 21, 2048),
+]
