@@ -44,8 +44,9 @@ def _join_quiet(fut) -> None:
 
 class TcpRingEngine:
     def __init__(self, tx: FrameSocket, rx: FrameSocket, rank: int, world: int, device=None,
-                 chunk_bytes: int = 256 * 1024):
+                 chunk_bytes: int = 256 * 1024, recv_timeout: float | None = 60.0):
         self.tx, self.rx = tx, rx
+        rx.sock.settimeout(recv_timeout)  # RecvTimeout of collective.py:333
         self.rank, self.world = rank, world
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.chunk_bytes = chunk_bytes

@@ -50,6 +50,7 @@ def replay(run, rx_stream: bytes, prefix: bytes = b"") -> bytes:
     def writer():
         try:
             c.sendall(prefix + rx_stream)
+            c.shutdown(socket.SHUT_WR)
         except OSError:
             pass
 
