@@ -15,12 +15,16 @@ import socket
 import struct
 from dataclasses import dataclass
 
+COLLECTIVE_INIT_VOTE = 13  # MessageType (wire.py:71)
+COLLECTIVE_COMPLETE_VOTE = 14  # MessageType (wire.py:72)
 CHUNK_DATA = 15  # MessageType.CHUNK_DATA (wire.py:73)
 QUANT_META = 17  # MessageType.QUANT_META (wire.py:75)
 
 _FRAME = struct.Struct(">IB")
 _CHUNK = struct.Struct(">QQIQI")
 _QMETA = struct.Struct(">QQIff")
+_INIT = struct.Struct(">QQBBB")
+_COMPLETE = struct.Struct(">QQBQQ")
 FRAME_OVERHEAD = _FRAME.size  # 5
 CHUNK_HEADER_LEN = _CHUNK.size  # 32
 QUANT_META_LEN = _QMETA.size  # 28
@@ -67,6 +71,49 @@ class QuantMeta:
         if len(buf) != QUANT_META_LEN:
             raise ProtocolError("bad QuantMeta length")
         return cls(*_QMETA.unpack(bytes(buf)))
+
+
+@dataclass
+class CollectiveInitVote:
+    """wire.py:754-773: the op descriptor every peer votes on before an
+    attempt (dtype 1 f32 / 2 f64, op 1..4 as ReduceOpCode)."""
+
+    tag: int
+    element_count: int
+    dtype: int
+    op: int
+    quantize: bool
+
+    def pack(self) -> bytes:
+        return _INIT.pack(self.tag, self.element_count, self.dtype, self.op, 1 if self.quantize else 0)
+
+    @classmethod
+    def unpack(cls, buf) -> "CollectiveInitVote":
+        if len(buf) != _INIT.size:
+            raise ProtocolError("bad CollectiveInitVote length")
+        tag, count, dtype, op, quant = _INIT.unpack(bytes(buf))
+        return cls(tag, count, dtype, op, bool(quant))
+
+
+@dataclass
+class CollectiveCompleteVote:
+    """wire.py:776-794: outcome vote with the attempt's payload counters."""
+
+    tag: int
+    seq_nr: int
+    ok: bool
+    tx_bytes: int = 0
+    rx_bytes: int = 0
+
+    def pack(self) -> bytes:
+        return _COMPLETE.pack(self.tag, self.seq_nr, 1 if self.ok else 0, self.tx_bytes, self.rx_bytes)
+
+    @classmethod
+    def unpack(cls, buf) -> "CollectiveCompleteVote":
+        if len(buf) != _COMPLETE.size:
+            raise ProtocolError("bad CollectiveCompleteVote length")
+        tag, seq, ok, tx, rx = _COMPLETE.unpack(bytes(buf))
+        return cls(tag, seq, bool(ok), tx, rx)
 
 
 def frame_header(msg_type: int, payload_len: int) -> bytes:

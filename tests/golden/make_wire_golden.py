@@ -126,6 +126,12 @@ def codec_goldens():
         "frame_chunk": wire.encode_frame(wire.MessageType.CHUNK_DATA, hdr.pack() + b"abcdefghijkl").hex(),
         "frame_meta": wire.encode_frame(wire.MessageType.QUANT_META, qm.pack()).hex(),
         "frame_empty": wire.encode_frame(wire.MessageType.CHUNK_DATA, b"").hex(),
+        "init_vote": wire.CollectiveInitVote(8, 1 << 20, wire.DType.F32, wire.ReduceOpCode.AVG, True).pack().hex(),
+        "init_vote_f64": wire.CollectiveInitVote(2**63 + 5, 3, wire.DType.F64, wire.ReduceOpCode.MIN, False).pack().hex(),
+        "complete_vote": wire.CollectiveCompleteVote(8, 2, True, 100, 101).pack().hex(),
+        "complete_vote_fail": wire.CollectiveCompleteVote(9, 7, False).pack().hex(),
+        "init_vote_type": int(wire.MessageType.COLLECTIVE_INIT_VOTE),
+        "complete_vote_type": int(wire.MessageType.COLLECTIVE_COMPLETE_VOTE),
         "chunk_data": int(wire.MessageType.CHUNK_DATA),
         "quant_meta_type": int(wire.MessageType.QUANT_META),
     }

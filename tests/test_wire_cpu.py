@@ -30,6 +30,21 @@ def test_codec_matches_reference_bytes():
     assert wire.QuantMeta.unpack(bytes.fromhex(g["quant_meta"])) == qm
 
 
+def test_vote_codecs_match_reference_bytes():
+    g = META["codec"]
+    v = wire.CollectiveInitVote(8, 1 << 20, 1, 2, True)
+    assert v.pack().hex() == g["init_vote"] and wire.CollectiveInitVote.unpack(v.pack()) == v
+    v = wire.CollectiveInitVote(2**63 + 5, 3, 2, 4, False)
+    assert v.pack().hex() == g["init_vote_f64"] and wire.CollectiveInitVote.unpack(v.pack()) == v
+    c = wire.CollectiveCompleteVote(8, 2, True, 100, 101)
+    assert c.pack().hex() == g["complete_vote"] and wire.CollectiveCompleteVote.unpack(c.pack()) == c
+    c = wire.CollectiveCompleteVote(9, 7, False)
+    assert c.pack().hex() == g["complete_vote_fail"] and wire.CollectiveCompleteVote.unpack(c.pack()) == c
+    assert (wire.COLLECTIVE_INIT_VOTE, wire.COLLECTIVE_COMPLETE_VOTE) == (g["init_vote_type"], g["complete_vote_type"])
+    with pytest.raises(wire.ProtocolError):
+        wire.CollectiveCompleteVote.unpack(b"\0" * 3)
+
+
 def _frames(stream: bytes):
     off = 0
     while off < len(stream):
