@@ -52,7 +52,7 @@ struct HashEntry {
 
 struct HashBatch {
   uint32_t count;
-  uint32_t pad;
+  uint32_t dynamic;  // 1: items from an atomic counter (list scheduling), 0: grid-stride
   HashEntry e[kMaxBatch];
 };
 
@@ -136,17 +136,22 @@ __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t ava
 // LANES*4-byte slice of ROWS consecutive 1 KiB rounds. TMA2D: stages are
 // filled by one 2-D tensor copy; otherwise (LANES == 256 only) by one 1-D
 // bulk copy of ROWS contiguous KiB.
-template <int LANES_, int ROWS_, int STAGES_, bool TMA2D_>
+template <int LANES_, int ROWS_, int STAGES_, bool TMA2D_, bool PROD_ = false>
 struct HashCfg {
   static constexpr int LANES = LANES_;
   static constexpr int ROWS = ROWS_;
   static constexpr int STAGES = STAGES_;
   static constexpr bool TMA2D = TMA2D_;
+  // PROD: one extra warp issues the TMA stages; the lane warps release slots
+  // through per-slot "empty" mbarriers instead of a CTA-wide barrier per stage
+  static constexpr bool PROD = PROD_;
+  static constexpr int THREADS = LANES + (PROD ? 32 : 0);
   static constexpr int GROUPS = 256 / LANES;
   static constexpr int SLICE = LANES * 4;
   static constexpr int STAGE_BYTES = ROWS * SLICE;
   static constexpr int SMEM = STAGE_BYTES * STAGES;
   static_assert(TMA2D || LANES == 256, "1-D bulk stages need whole rounds");
+  static_assert(!PROD || TMA2D, "the producer warp issues 2-D TMA boxes");
 };
 
 // Run lanes [lane0, lane0 + LANES) of one segment; h is the lane's state.
@@ -215,6 +220,72 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
   return h;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// hash_group with a producer warp (C::PROD, blockDim = LANES + 32). Thread
+// LANES issues every stage of the lane group into a ring slot once the lane
+// warps released it (empty[slot], one arrival per lane warp); lane warps wait
+// for full[slot] and never synchronise with each other, so one slow warp no
+// longer holds the other three at a per-stage __syncthreads. `g` numbers the
+// stages of the whole launch (it carries over from one entry to the next), so
+// slot = g % STAGES and the mbarrier phase parity is (g / STAGES) & 1.
+template <class C>
+__device__ __forceinline__ uint64_t hash_group_prod(const uint8_t *p, uint64_t nbytes,
+                                                    const CUtensorMap *map, uint32_t lane0,
+                                                    uint64_t h, uint8_t *stage, uint64_t *full,
+                                                    uint64_t *empty, uint32_t &g) {
+  const int tid = threadIdx.x;
+  const bool producer = tid >= C::LANES;
+  const uint32_t lane = lane0 + tid;
+  const uint64_t full_words = nbytes >> 2;
+  const uint64_t rounds = full_words >> 8;
+  if (rounds > 0 && map != nullptr) {
+    const uint32_t nst = (uint32_t)((rounds + C::ROWS - 1) / C::ROWS);
+    if (producer) {
+      if (tid == C::LANES) {
+        tensormap_acquire(map);
+        for (uint32_t s = 0; s < nst; ++s) {
+          const uint32_t G = g + s, slot = G % C::STAGES;
+          if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
+          mbar_expect_tx(&full[slot], C::STAGE_BYTES);
+          tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(s * C::ROWS), &full[slot]);
+        }
+      }
+    } else {
+      for (uint32_t s = 0; s < nst; ++s) {
+        const uint32_t G = g + s, slot = G % C::STAGES;
+        mbar_wait(&full[slot], (G / C::STAGES) & 1u);
+        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
+        const uint64_t left = rounds - (uint64_t)s * C::ROWS;
+        Fnv f(h);
+        if (left >= (uint64_t)C::ROWS) {
+#pragma unroll
+          for (int r = 0; r < C::ROWS; ++r) f.step(wds[r * C::LANES]);
+        } else {
+          const int nr = (int)left;
+          for (int r = 0; r < nr; ++r) f.step(wds[r * C::LANES]);
+        }
+        h = f.value();
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+      }
+    }
+    g += nst;
+  } else if (!producer) {
+    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
+  }
+  if (producer) return 0;
+  const uint64_t done = rounds << 8;
+  const uint64_t rem = full_words - done;  // < 256
+  const uint8_t *q = p + done * 4;
+  if ((uint64_t)lane < rem) h = fnv_step(h, load_word_any(q + 4 * lane, 4));
+  const uint32_t tail = (uint32_t)(nbytes & 3);
+  if (tail && (uint64_t)lane == rem) h = fnv_step(h, load_word_any(q + 4 * lane, tail));
+  return h;
+}
+
 // depth-8 tree over 256 lanes in shared memory (pairs (2j, 2j+1), lower is a);
 // CTA size >= 64; returns the root in every thread
 __device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s) {
@@ -232,37 +303,59 @@ __device__ __forceinline__ uint64_t tree_fold(uint64_t *lane_s) {
   return lane_s[0];
 }
 
-template <int STAGES>
+template <class C>
 __device__ __forceinline__ void init_bars(uint64_t *bars) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+    if constexpr (C::PROD)
+      for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[C::STAGES + s], C::LANES / 32);
     mbar_fence_init();
   }
   __syncthreads();
 }
 
+template <class C>
+__device__ __forceinline__ uint64_t hash_any(const uint8_t *p, uint64_t nbytes, const CUtensorMap *map,
+                                             uint32_t lane0, uint64_t h, uint8_t *stage, uint64_t *bars,
+                                             uint32_t &sync) {
+  if constexpr (C::PROD)
+    return hash_group_prod<C>(p, nbytes, map, lane0, h, stage, bars, bars + C::STAGES, sync);
+  else
+    return hash_group<C>(p, nbytes, map, lane0, h, stage, bars, sync);
+}
+
 // Work item = (entry, lane group); the last group of an entry folds.
 template <class C>
-__global__ void __launch_bounds__(C::LANES)
+__global__ void __launch_bounds__(C::THREADS)
     simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *arrived) {
   extern __shared__ __align__(1024) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[C::STAGES];
+  __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
   __shared__ uint64_t lane_s[256];
   __shared__ uint32_t s_last;
-  init_bars<C::STAGES>(bars);
+  init_bars<C>(bars);
   uint32_t parity = 0;
   const uint32_t items = b.count * C::GROUPS;
-  for (uint32_t it = blockIdx.x; it < items; it += gridDim.x) {
+  // dynamic list scheduling: items are taken in LPT order (largest entries
+  // first) by whichever CTA is free, from a counter behind the arrival counts
+  uint32_t *next = arrived + b.count;
+  __shared__ uint32_t s_item;
+  for (uint32_t k = 0;; ++k) {
+    if (b.dynamic) {
+      if (threadIdx.x == 0) s_item = atomicAdd(next, 1u);
+      __syncthreads();
+    }
+    const uint32_t it = b.dynamic ? s_item : blockIdx.x + k * gridDim.x;
+    if (it >= items) break;
     const uint32_t e = it / C::GROUPS, g = it % C::GROUPS;
     const HashEntry E = b.e[e];
     const uint32_t lane0 = g * C::LANES;
-    uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, parity);
+    uint64_t h = hash_any<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, parity);
     if constexpr (C::GROUPS == 1) {
-      lane_s[threadIdx.x] = h;
+      if (threadIdx.x < C::LANES) lane_s[threadIdx.x] = h;
       uint64_t root = tree_fold(lane_s);
       if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
     } else {
-      lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
+      if (threadIdx.x < C::LANES) lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) s_last = (atomicAdd(&arrived[e], 1u) == C::GROUPS - 1) ? 1u : 0u;
@@ -281,17 +374,17 @@ __global__ void __launch_bounds__(C::LANES)
 
 // streaming update of one segment: grid = GROUPS CTAs, lane state in/out
 template <class C>
-__global__ void __launch_bounds__(C::LANES)
+__global__ void __launch_bounds__(C::THREADS)
     simplehash_update_kernel(uint64_t *state, const uint8_t *p, uint64_t nbytes,
                              const __grid_constant__ CUtensorMap map, int have_map) {
   extern __shared__ __align__(1024) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bars[C::STAGES];
-  init_bars<C::STAGES>(bars);
+  __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
+  init_bars<C>(bars);
   uint32_t parity = 0;
-  const uint32_t lane = blockIdx.x * C::LANES + threadIdx.x;
-  uint64_t h = hash_group<C>(p, nbytes, have_map ? &map : nullptr, blockIdx.x * C::LANES,
-                             state[lane], stage, bars, parity);
-  state[lane] = h;
+  const uint32_t lane = blockIdx.x * C::LANES + (threadIdx.x % C::LANES);
+  uint64_t h = hash_any<C>(p, nbytes, have_map ? &map : nullptr, blockIdx.x * C::LANES,
+                           state[lane], stage, bars, parity);
+  if (threadIdx.x < C::LANES) state[lane] = h;
 }
 
 __global__ void simplehash_init_kernel(uint64_t *state) { state[threadIdx.x] = kFnvOffset; }
@@ -304,22 +397,28 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
-// Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default)
-// measured on B200 (config-4 layout / one 1.05 GB entry / 64 x 64 MiB):
-//   <128,64,3>  12.1 ms /  99 GB/s / 5.64 TB/s   (2-D TMA, 2 CTAs/entry)
-//   <128,32,6>  13.4 ms /  84 GB/s / 4.90 TB/s
-//   <64,64,4>   11.6 ms /  98 GB/s / 4.04 TB/s
-//   <256,16,6>  22.0 ms /  47 GB/s / 2.61 TB/s   (1-D bulk, 1 CTA/entry)
-// ncu on <128,64,3>: 23% of warp samples wait on the stage mbarrier, i.e.
-// the large entries are short of bytes in flight -> deeper rings below.
-using HashV0 = HashCfg<128, 64, 3, true>;
-using HashV1 = HashCfg<128, 64, 6, true>;   // 192 KiB ring, 1 CTA/SM
-using HashV2 = HashCfg<64, 128, 4, true>;   // 4 CTAs/entry, 128 KiB ring
-using HashV3 = HashCfg<64, 64, 6, true>;    // 4 CTAs/entry, 96 KiB ring
-// Entries that would outlast the whole batch at the shared-SM rate get SMs of
-// their own: 4 lane groups of 64 (2 warps, chain-latency-bound) and a 192 KiB
-// ring, which by itself keeps any other CTA off that SM.
-using HashBig = HashCfg<64, 128, 6, true>;
+// Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default),
+// measured on B200 with list scheduling (config-4 layout / one 1.05 GB entry /
+// 64 x 64 MiB, tools/hash_variants.py, median of 7):
+//   <128,128,3,P>  8.5 ms / 131 GB/s / 7.1 TB/s   (default)
+//   <64,128,4,P>   8.2 ms / 128 GB/s / 4.0 TB/s   (64 lanes per SM: HBM-starved)
+//   <128,64,3>    12.5 ms / 111 GB/s / 6.7 TB/s   (no producer warp; 10.6 ms grid-stride)
+//   <128,96,4,P>   9.0 ms / 123 GB/s / 7.1 TB/s
+// One entry is bounded by its lane chain (14.5 cycles per LOP3->IMAD.WIDE
+// step with the hi side interleaved, tools/micro/chain_lds.cu): 1 KiB per step
+// => 139 GB/s, 7.6 ms for the 1.05 GB embedding. Deep stages (128 rows) keep
+// ~2 us of TMA lookahead per CTA and amortise the per-stage handshakes.
+using HashV0 = HashCfg<128, 128, 3, true, true>;
+using HashV1 = HashCfg<64, 128, 4, true, true>;
+using HashV2 = HashCfg<128, 64, 3, true>;
+using HashV3 = HashCfg<128, 96, 4, true, true>;
+static bool hash_dynamic() {
+  static bool on = [] {
+    const char *e = getenv("PCCLB_HASH_DYN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int hash_variant() {
   static int v = [] {
@@ -392,7 +491,6 @@ static int prepare_hash_kernels() {
   if (!rc) rc = prepare_variant<HashV1>();
   if (!rc) rc = prepare_variant<HashV2>();
   if (!rc) rc = prepare_variant<HashV3>();
-  if (!rc) rc = prepare_variant<HashBig>();
   if (rc) return rc;
   if (dev >= 0 && dev < 64) done[dev] = true;
   return PCCLB_OK;
@@ -405,13 +503,13 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   if (count == 0) return PCCLB_OK;
   int occ = 0;
   PCCLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, simplehash_batch_kernel<C>,
-                                                           C::LANES, C::SMEM));
+                                                           C::THREADS, C::SMEM));
   if (occ < 1) occ = 1;
   const uint32_t slots = (uint32_t)(sm_count() * occ);
   // per-launch device scratch: lane values, arrival counters, tensor maps
   const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
   const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  const size_t cnt_bytes = ((size_t)m_max * sizeof(uint32_t) + 127) & ~size_t(127);
+  const size_t cnt_bytes = ((size_t)(m_max + 1) * sizeof(uint32_t) + 127) & ~size_t(127);
   const size_t map_bytes = C::TMA2D ? (size_t)m_max * sizeof(CUtensorMap) : 0;
   char *scratch = nullptr;
   PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), lanes_bytes + cnt_bytes + map_bytes, s));
@@ -436,6 +534,7 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       }
     }
     batch.count = m;
+    batch.dynamic = hash_dynamic() ? 1u : 0u;
     for (uint32_t i = 0; i < m; ++i) {
       const uint32_t k = order[base + i];
       HashEntry &E = batch.e[i];
@@ -450,13 +549,13 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       e = cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
       if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
     }
-    if (e == cudaSuccess && C::GROUPS > 1) e = cudaMemsetAsync(arrived, 0, m * sizeof(uint32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(arrived, 0, (m + 1) * sizeof(uint32_t), s);
     if (e != cudaSuccess) {
       rc = cuda_status(e);
       break;
     }
     unsigned grid = std::min<uint32_t>(m * C::GROUPS, slots);
-    simplehash_batch_kernel<C><<<grid, C::LANES, C::SMEM, s>>>(batch, lanes, arrived);
+    simplehash_batch_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(batch, lanes, arrived);
     e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_status(e);
   }
@@ -465,40 +564,12 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   return rc;
 }
 
-// per-device side stream + events for the big/rest split (one per host thread)
-struct Fork {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static Fork &fork_for_device() {
-  static thread_local Fork forks[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Fork &f = forks[dev & 63];
-  if (!f.side) {
-    if (cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess)
-      f.side = nullptr;
-  }
-  return f;
-}
-
-// PCCLB_HASH_BIG=0 disables the big-entry split (for measurements)
-static bool big_entries_enabled() {
-  static bool on = [] {
-    const char *e = getenv("PCCLB_HASH_BIG");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 template <class C>
 static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaStream_t s) {
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   int have = (C::TMA2D && encode_map<C>(&map, d, nbytes)) ? 1 : 0;
-  simplehash_update_kernel<C><<<C::GROUPS, C::LANES, C::SMEM, s>>>(
+  simplehash_update_kernel<C><<<C::GROUPS, C::THREADS, C::SMEM, s>>>(
       state, static_cast<const uint8_t *>(d), nbytes, map, have);
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
@@ -524,42 +595,16 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
   cudaStream_t s = as_stream(stream);
-  // big entries: chain time at the shared rate (~100 GB/s) beyond the batch's
-  // HBM time (total / ~6 TB/s), i.e. more than 1/64 of the bytes
-  uint64_t total = 0;
-  for (uint32_t i = 0; i < count; ++i) total += h_nbytes[i];
-  std::vector<uint32_t> big, rest;
-  for (uint32_t k : order) {
-    const bool is_big = big_entries_enabled() && big.size() < 16 && h_nbytes[k] >= (64ull << 20) &&
-                        h_nbytes[k] > total / 64 && count > 1;
-    (is_big ? big : rest).push_back(k);
+  switch (hash_variant()) {
+    case 1:
+      return launch_batches<HashV1>(order, h_ptrs, h_nbytes, d_out, s);
+    case 2:
+      return launch_batches<HashV2>(order, h_ptrs, h_nbytes, d_out, s);
+    case 3:
+      return launch_batches<HashV3>(order, h_ptrs, h_nbytes, d_out, s);
+    default:
+      return launch_batches<HashV0>(order, h_ptrs, h_nbytes, d_out, s);
   }
-  auto launch_rest = [&](cudaStream_t st) {
-    switch (hash_variant()) {
-      case 1:
-        return launch_batches<HashV1>(rest, h_ptrs, h_nbytes, d_out, st);
-      case 2:
-        return launch_batches<HashV2>(rest, h_ptrs, h_nbytes, d_out, st);
-      case 3:
-        return launch_batches<HashV3>(rest, h_ptrs, h_nbytes, d_out, st);
-      default:
-        return launch_batches<HashV0>(rest, h_ptrs, h_nbytes, d_out, st);
-    }
-  };
-  if (big.empty()) return launch_rest(s);
-  // the big entries start first on `s`; the rest runs beside them on a side
-  // stream forked from and joined back into `s`
-  Fork &f = fork_for_device();
-  if (!f.side) return PCCLB_ECUDA;
-  rc = launch_batches<HashBig>(big, h_ptrs, h_nbytes, d_out, s);
-  if (rc) return rc;
-  PCCLB_CUDA(cudaEventRecord(f.fork, s));
-  PCCLB_CUDA(cudaStreamWaitEvent(f.side, f.fork, 0));
-  rc = launch_rest(f.side);
-  if (rc) return rc;
-  PCCLB_CUDA(cudaEventRecord(f.join, f.side));
-  PCCLB_CUDA(cudaStreamWaitEvent(s, f.join, 0));
-  return PCCLB_OK;
 }
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {

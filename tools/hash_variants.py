@@ -17,18 +17,26 @@ from paper_2505_14065_b200.sharedstate import simplehash_many_async  # noqa: E40
 
 
 def timeit(views, reps=5):
+    """Per-call CUDA-event times; reports the median and the min."""
+    import time
+
     out = torch.empty(len(views), dtype=torch.int64, device="cuda")
     simplehash_many_async(views, out)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    host = []
+    ev[0].record()
+    for i in range(reps):
+        t0 = time.perf_counter()
         simplehash_many_async(views, out)
-    b.record()
+        host.append((time.perf_counter() - t0) * 1e3)
+        ev[i + 1].record()
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+    ts = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(reps))
+    ms = ts[len(ts) // 2]
     nb = sum(v.numel() * v.element_size() for v in views)
-    return {"ms": round(ms, 3), "GBps": round(nb / ms / 1e6, 1)}, out.cpu().tolist()
+    return {"ms": round(ms, 3), "GBps": round(nb / ms / 1e6, 1), "min_ms": round(ts[0], 3),
+            "max_ms": round(ts[-1], 3), "host_ms": round(max(host), 3)}, out.cpu().tolist()
 
 
 layout = llama3_8b_layout()
@@ -39,10 +47,10 @@ views, off = [], 0
 for _, n in layout:
     views.append(state[off : off + n])
     off += n
-res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0")), "big": os.environ.get("PCCLB_HASH_BIG", "1")}
-res["config4"], digests = timeit(views)
-res["single_1GB"], _ = timeit([views[0]], 3)
+res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0"))}
+res["config4"], digests = timeit(views, 7)
+res["single_1GB"], _ = timeit([views[0]], 5)
 eq = state[: 64 * (32 << 20)].view(64, -1)
-res["64x64MiB"], _ = timeit([eq[i] for i in range(64)])
+res["64x64MiB"], _ = timeit([eq[i] for i in range(64)], 7)
 res["digest0"] = digests[0] & 0xFFFFFFFFFFFFFFFF
 print(json.dumps(res))
