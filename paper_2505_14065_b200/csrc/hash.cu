@@ -5,21 +5,37 @@
 // offset basis; lanes fold by a depth-8 tree (a ^ rotl(b, 27)) * P over pairs
 // (2j, 2j+1); root ^ byte length.
 //
-// Bounds (measured, tools/micro/chain_micro.cu): one FNV step is a dependent
-// LOP3 -> IMAD.WIDE pair of ~14.3 cycles, so one entry (256 chains) cannot go
-// faster than 1 KiB per 14.3 cycles (~141 GB/s at 1.97 GHz) however many SMs
-// it gets; an SM issues at most ~1 KiB of steps per ~13.4 cycles (~150 GB/s),
-// so the whole chip (~22 TB/s) is far above HBM. Many entries in flight are
-// therefore HBM-bound, and the largest entry sets a latency floor.
+// Bounds (measured on B200, tools/micro/chain_lds.cu): one FNV step fed from
+// shared memory costs 14.5 cycles when the lane also carries the hi half, and
+// 10.5 cycles for the 32-bit lo chain alone (LOP3 -> IMAD, one cross-pipe hop
+// each way). One entry has only 256 chains, so it cannot go faster than 1 KiB
+// per step however many SMs it gets (139 GB/s full step, 192 GB/s lo only);
+// many entries in flight are HBM-bound, and the largest entry sets a floor.
 //
-// Mapping (default): an entry's 256 lanes are split over kGroups = 2 CTAs of
-// 128 threads (thread t = lane 128g + t), each on its own SM, so a lone large
-// entry runs at its chain bound. A CTA streams its 512-byte slice of every
-// 1 KiB round through a 3-stage shared-memory ring; each stage (64 rounds) is
-// ONE 2-D TMA copy (cp.async.bulk.tensor.2d, the entry viewed as a
-// [rounds x 256] u32 tensor, box 128 x 64) completing on an mbarrier.
-// Entries are dealt largest first, so the longest chains start first; the
-// last group of an entry to finish runs the tree fold.
+// Mapping: an entry's 256 lanes are split over GROUPS = 2 lane groups of 128;
+// a work item is one lane group of one entry (or of one segment, below) and
+// runs on one CTA of 4 lane warps + 1 producer warp. The producer streams the
+// group's 512-byte slice of 128 consecutive 1 KiB rounds per 2-D TMA box
+// (cp.async.bulk.tensor.2d over the entry viewed as [rounds x 256] u32) into a
+// 3-stage shared-memory ring; lane warps release slots through per-slot
+// mbarriers. Items are handed out by an atomic counter in LPT order (largest
+// entries first) -- list scheduling -- and the last group of an entry folds.
+//
+// Two-phase path for entries whose chain outlasts the rest of the batch
+// ("big" entries, e.g. config 4's 1.05 GB embedding and LM head). The FNV step
+// splits into lo' = (lo ^ w) * 435 mod 2^32, which depends on lo alone, and
+// hi' = 435 hi + umulhi(x, 435) + (x << 8) with x = lo ^ w, which is affine in
+// hi. So:
+//   phase 1 (one item per lane group): run only the lo chain over the whole
+//     entry (10.5 instead of 14.5 cycles per step) and publish lo at every
+//     kSegRows-row checkpoint;
+//   phase 2 (one item per segment and lane group, run by any free CTA as soon
+//     as its checkpoint is published): rerun the full step over the segment
+//     from (lo = checkpoint, hi = 0), which leaves hi = A_j, the segment's
+//     additive term;
+//   combine (by the last finisher): hi = 435^m_j * hi + A_j over the segments,
+//     h = hi:lo_final, then the tail words and the tree fold.
+// Phase 2 reads the entry a second time, in parallel on otherwise idle SMs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -37,22 +53,29 @@ namespace pcclb {
 
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kMaxBatch = 1000;  // HashBatch must fit the 32 KiB kernel-parameter space
-#ifndef HASH_UNROLL
-#define HASH_UNROLL 0  // 0: fully unrolled (measured best: 64 > 32 > 16 > 8)
-#endif
-constexpr int kHashUnroll = HASH_UNROLL;  // unroll of the per-stage chain loop  // HashBatch must fit the 32 KiB kernel-parameter space
+constexpr uint32_t kSegRows = 4096;  // checkpoint spacing of the two-phase path (rows of 1 KiB)
+constexpr uint32_t kMaxBig = 16;     // big entries per launch
+constexpr int kMaxBatch = 640;       // HashBatch must fit the 32 KiB kernel-parameter space
 
 struct HashEntry {
   const uint8_t *ptr;
   uint64_t nbytes;
   uint64_t *out;
-  const CUtensorMap *map;  // 2-D view [rounds x 256] u32, or null (fallback loads)
+  const CUtensorMap *map;  // 2-D view [rounds x 256] u32, or null (direct loads)
+  uint32_t *aux;           // big entries: [nseg x 256] checkpoints, [256] final lo, [nseg x 256] A
+  uint32_t nseg;           // big entries: number of kSegRows segments
+  uint32_t pad;
 };
 
+// Entries [0, nbig) are big (two-phase); item space:
+//   [0, nbig*G)                         phase-1 lo chains
+//   [nbig*G, count*G)                   ordinary entries
+//   [count*G, count*G + segmax*nbig*G)  phase-2 segments, segment-major
 struct HashBatch {
   uint32_t count;
-  uint32_t dynamic;  // 1: items from an atomic counter (list scheduling), 0: grid-stride
+  uint32_t nbig;
+  uint32_t segmax;
+  uint32_t pad;
   HashEntry e[kMaxBatch];
 };
 
@@ -70,6 +93,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -77,14 +103,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *map, int x, int y,
@@ -98,13 +116,16 @@ __device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *map, in
 __device__ __forceinline__ void tensormap_acquire(const CUtensorMap *map) {
   asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(map) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // One FNV-1a-64 step h = (h ^ w) * P on the split state (lo, hi).
 // P = 2^40 + 435 and w is a zero-extended u32, so with x = lo ^ w:
 //   lo' = (x * 435) mod 2^32
 //   hi' = hi * 435 + floor(x * 435 / 2^32) + (x << 8)     (mod 2^32)
-// The loop-carried paths are LOP3 -> IMAD.WIDE on lo and a single IMAD on hi
-// (the x-dependent addend is computed off the hi chain).
 struct Fnv {
   uint32_t lo, hi;
   __device__ __forceinline__ explicit Fnv(uint64_t h) : lo((uint32_t)h), hi((uint32_t)(h >> 32)) {}
@@ -117,11 +138,23 @@ struct Fnv {
     // explicit mad so the compiler cannot re-associate x-terms onto the hi chain
     asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hi) : "r"(hi), "r"(add));
   }
+  // phase 1 of the two-phase path: the lo chain alone
+  __device__ __forceinline__ void step_lo(uint32_t w) { lo = (lo ^ w) * 435u; }
 };
 __device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint32_t w) {
   return (h ^ (uint64_t)w) * kFnvPrime;
 }
 __device__ __forceinline__ uint64_t rotl27(uint64_t v) { return (v << 27) | (v >> 37); }
+// 435^m mod 2^32
+__device__ __forceinline__ uint32_t pow435(uint32_t m) {
+  uint32_t r = 1, b = 435u;
+  while (m) {
+    if (m & 1u) r *= b;
+    b *= b;
+    m >>= 1;
+  }
+  return r;
+}
 
 // little-endian u32 at an arbitrary byte address (zero beyond `avail` bytes)
 __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t avail) {
@@ -131,159 +164,127 @@ __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t ava
   return w;
 }
 
-// Kernel shape: LANES threads per CTA (thread t = lane lane0 + t), a ring of
-// STAGES shared-memory stages of ROWS rounds each; a stage holds the CTA's
-// LANES*4-byte slice of ROWS consecutive 1 KiB rounds. TMA2D: stages are
-// filled by one 2-D tensor copy; otherwise (LANES == 256 only) by one 1-D
-// bulk copy of ROWS contiguous KiB.
-template <int LANES_, int ROWS_, int STAGES_, bool TMA2D_, bool PROD_ = false>
+// CTA shape: LANES lane threads (thread t = lane lane0 + t) plus one producer
+// warp; a ring of STAGES shared-memory stages, each the group's LANES*4-byte
+// slice of ROWS consecutive 1 KiB rounds (one 2-D TMA box).
+template <int LANES_, int ROWS_, int STAGES_>
 struct HashCfg {
   static constexpr int LANES = LANES_;
   static constexpr int ROWS = ROWS_;
   static constexpr int STAGES = STAGES_;
-  static constexpr bool TMA2D = TMA2D_;
-  // PROD: one extra warp issues the TMA stages; the lane warps release slots
-  // through per-slot "empty" mbarriers instead of a CTA-wide barrier per stage
-  static constexpr bool PROD = PROD_;
-  static constexpr int THREADS = LANES + (PROD ? 32 : 0);
+  static constexpr int THREADS = LANES + 32;
+  static constexpr int WARPS = LANES / 32;
   static constexpr int GROUPS = 256 / LANES;
-  static constexpr int SLICE = LANES * 4;
-  static constexpr int STAGE_BYTES = ROWS * SLICE;
+  static constexpr int STAGE_BYTES = ROWS * LANES * 4;
   static constexpr int SMEM = STAGE_BYTES * STAGES;
-  static_assert(TMA2D || LANES == 256, "1-D bulk stages need whole rounds");
-  static_assert(!PROD || TMA2D, "the producer warp issues 2-D TMA boxes");
+  static_assert(kSegRows % ROWS == 0, "segments are whole stages");
 };
+// Measured (config-4 layout / one 1.05 GB entry / 64 x 64 MiB, full steps,
+// tools/hash_variants.py): <128,128,3> 8.5 ms / 131 GB/s / 7.1 TB/s;
+// <64,128,4> 8.2 ms / 128 GB/s / 4.0 TB/s (64 lanes per SM starve HBM);
+// <128,96,4> 9.0 ms; <128,64,3> without the producer warp 10.6 ms. Deep
+// stages keep ~2 us of TMA lookahead per CTA and amortise the handshakes.
+using HashC = HashCfg<128, 128, 3>;
 
-// Run lanes [lane0, lane0 + LANES) of one segment; h is the lane's state.
-// Must be called by all threads of the CTA (uses __syncthreads).
-template <class C>
-__device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes,
-                                               const CUtensorMap *map, uint32_t lane0, uint64_t h,
-                                               uint8_t *stage, uint64_t *bars, uint32_t &parity) {
+// Rows [row0, row0 + nrows) of lanes [lane0, lane0 + LANES) through the TMA
+// ring; h is the lane's state (lane threads). The producer thread (thread
+// LANES) issues a stage into slot g % STAGES once the lane warps released it
+// (empty[slot], one arrival per lane warp); `g` numbers the stages of the whole
+// launch, so the mbarrier phase parity is (g / STAGES) & 1. LO_ONLY: step the
+// lo chain only and, every kSegRows rows (row0 = 0), store the lo value that
+// starts the segment to ck[seg * 256 + lane] and count it in *progress.
+template <class C, bool LO_ONLY>
+__device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t lane0, uint64_t row0,
+                                             uint64_t nrows, uint64_t h, uint8_t *stage,
+                                             uint64_t *full, uint64_t *empty, uint32_t &g,
+                                             uint32_t *ck, uint32_t *progress) {
   const int tid = threadIdx.x;
-  const uint32_t lane = lane0 + tid;
-  const uint64_t full_words = nbytes >> 2;
-  const uint64_t rounds = full_words >> 8;
-  const bool fast = rounds > 0 && (C::TMA2D ? map != nullptr : ((uintptr_t)p & 15) == 0);
-  if (fast) {
-    const uint64_t nst = (rounds + C::ROWS - 1) / C::ROWS;
-    auto issue = [&](uint64_t s, int slot) {  // called by thread 0
-      uint8_t *dst = stage + slot * C::STAGE_BYTES;
-      if constexpr (C::TMA2D) {
-        // out-of-range rows of the last box are zero-filled and still counted
-        mbar_expect_tx(&bars[slot], C::STAGE_BYTES);
-        tma_2d_g2s(dst, map, (int)lane0, (int)(s * C::ROWS), &bars[slot]);
-      } else {
-        const uint32_t rows = (uint32_t)min((uint64_t)C::ROWS, rounds - s * C::ROWS);
-        mbar_expect_tx(&bars[slot], rows * 1024);
-        bulk_g2s(dst, p + s * C::ROWS * 1024, rows * 1024, &bars[slot]);
+  const uint32_t nst = (uint32_t)((nrows + C::ROWS - 1) / C::ROWS);
+  if (tid >= C::LANES) {
+    if (tid == C::LANES) {
+      tensormap_acquire(map);
+      for (uint32_t s = 0; s < nst; ++s) {
+        const uint32_t G = g + s, slot = G % C::STAGES;
+        if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
+        // rows past the end of the tensor are zero-filled and still counted
+        mbar_expect_tx(&full[slot], C::STAGE_BYTES);
+        tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(row0 + (uint64_t)s * C::ROWS),
+                   &full[slot]);
       }
-    };
-    if (tid == 0) {
-      if constexpr (C::TMA2D) tensormap_acquire(map);
-      for (uint64_t s = 0; s < nst && s < (uint64_t)C::STAGES; ++s) issue(s, (int)s);
     }
-    for (uint64_t st = 0; st < nst; ++st) {
-      const int slot = (int)(st % C::STAGES);
-      mbar_wait(&bars[slot], (parity >> slot) & 1u);
-      parity ^= 1u << slot;
+  } else {
+    Fnv f(h);
+    for (uint32_t s = 0; s < nst; ++s) {
+      const uint32_t G = g + s, slot = G % C::STAGES;
+      if constexpr (LO_ONLY) {
+        if ((s * C::ROWS) % kSegRows == 0) {
+          ck[(s * C::ROWS / kSegRows) * 256 + lane0 + tid] = f.lo;
+          __syncwarp();
+          if ((tid & 31) == 0) {
+            __threadfence();
+            atomicAdd(progress, 1u);
+          }
+        }
+      }
+      mbar_wait(&full[slot], (G / C::STAGES) & 1u);
       const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
-      const uint64_t left = rounds - st * C::ROWS;
-      Fnv f(h);
+      const uint64_t left = nrows - (uint64_t)s * C::ROWS;
       if (left >= (uint64_t)C::ROWS) {
-        if constexpr (kHashUnroll == 0) {
-          // fully unrolled: the compiler hoists the shared-memory loads well
-          // ahead of the chain (config 4: 10.75 ms vs 11.85 ms at unroll 16)
+        // fully unrolled: the shared-memory loads are hoisted ahead of the chain
 #pragma unroll
-          for (int r = 0; r < C::ROWS; ++r) f.step(wds[r * C::LANES]);
-        } else {
-#pragma unroll kHashUnroll
-          for (int r = 0; r < C::ROWS; ++r) f.step(wds[r * C::LANES]);
+        for (int r = 0; r < C::ROWS; ++r) {
+          if constexpr (LO_ONLY)
+            f.step_lo(wds[r * C::LANES]);
+          else
+            f.step(wds[r * C::LANES]);
         }
       } else {
         const int nr = (int)left;
-        for (int r = 0; r < nr; ++r) f.step(wds[r * C::LANES]);
+        for (int r = 0; r < nr; ++r) {
+          if constexpr (LO_ONLY)
+            f.step_lo(wds[r * C::LANES]);
+          else
+            f.step(wds[r * C::LANES]);
+        }
       }
-      h = f.value();
-      __syncthreads();  // every lane done with this slot before it is refilled
-      if (tid == 0 && st + C::STAGES < nst) issue(st + C::STAGES, slot);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
     }
-  } else {
-    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
+    h = f.value();
   }
-  const uint64_t done = rounds << 8;
-  const uint64_t rem = full_words - done;  // < 256
-  const uint8_t *q = p + done * 4;
-  if ((uint64_t)lane < rem) h = fnv_step(h, load_word_any(q + 4 * lane, 4));
-  const uint32_t tail = (uint32_t)(nbytes & 3);
-  if (tail && (uint64_t)lane == rem) h = fnv_step(h, load_word_any(q + 4 * lane, tail));
+  g += nst;
   return h;
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// hash_group with a producer warp (C::PROD, blockDim = LANES + 32). Thread
-// LANES issues every stage of the lane group into a ring slot once the lane
-// warps released it (empty[slot], one arrival per lane warp); lane warps wait
-// for full[slot] and never synchronise with each other, so one slow warp no
-// longer holds the other three at a per-stage __syncthreads. `g` numbers the
-// stages of the whole launch (it carries over from one entry to the next), so
-// slot = g % STAGES and the mbarrier phase parity is (g / STAGES) & 1.
-template <class C>
-__device__ __forceinline__ uint64_t hash_group_prod(const uint8_t *p, uint64_t nbytes,
-                                                    const CUtensorMap *map, uint32_t lane0,
-                                                    uint64_t h, uint8_t *stage, uint64_t *full,
-                                                    uint64_t *empty, uint32_t &g) {
-  const int tid = threadIdx.x;
-  const bool producer = tid >= C::LANES;
-  const uint32_t lane = lane0 + tid;
+// the words after the whole rounds: lane < rem takes one full word, lane ==
+// rem the zero-padded tail (sharedstate.py:45-54)
+__device__ __forceinline__ uint64_t tail_steps(uint64_t h, const uint8_t *p, uint64_t nbytes,
+                                               uint32_t lane) {
   const uint64_t full_words = nbytes >> 2;
-  const uint64_t rounds = full_words >> 8;
-  if (rounds > 0 && map != nullptr) {
-    const uint32_t nst = (uint32_t)((rounds + C::ROWS - 1) / C::ROWS);
-    if (producer) {
-      if (tid == C::LANES) {
-        tensormap_acquire(map);
-        for (uint32_t s = 0; s < nst; ++s) {
-          const uint32_t G = g + s, slot = G % C::STAGES;
-          if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
-          mbar_expect_tx(&full[slot], C::STAGE_BYTES);
-          tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(s * C::ROWS), &full[slot]);
-        }
-      }
-    } else {
-      for (uint32_t s = 0; s < nst; ++s) {
-        const uint32_t G = g + s, slot = G % C::STAGES;
-        mbar_wait(&full[slot], (G / C::STAGES) & 1u);
-        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
-        const uint64_t left = rounds - (uint64_t)s * C::ROWS;
-        Fnv f(h);
-        if (left >= (uint64_t)C::ROWS) {
-#pragma unroll
-          for (int r = 0; r < C::ROWS; ++r) f.step(wds[r * C::LANES]);
-        } else {
-          const int nr = (int)left;
-          for (int r = 0; r < nr; ++r) f.step(wds[r * C::LANES]);
-        }
-        h = f.value();
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
-      }
-    }
-    g += nst;
-  } else if (!producer) {
-    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
-  }
-  if (producer) return 0;
-  const uint64_t done = rounds << 8;
+  const uint64_t done = (full_words >> 8) << 8;
   const uint64_t rem = full_words - done;  // < 256
   const uint8_t *q = p + done * 4;
   if ((uint64_t)lane < rem) h = fnv_step(h, load_word_any(q + 4 * lane, 4));
   const uint32_t tail = (uint32_t)(nbytes & 3);
   if (tail && (uint64_t)lane == rem) h = fnv_step(h, load_word_any(q + 4 * lane, tail));
   return h;
+}
+
+// All rounds of lanes [lane0, lane0 + LANES) plus the tail words, from state h.
+template <class C>
+__device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes,
+                                               const CUtensorMap *map, uint32_t lane0, uint64_t h,
+                                               uint8_t *stage, uint64_t *bars, uint32_t &g) {
+  const uint32_t lane = lane0 + threadIdx.x;
+  const uint64_t rounds = nbytes >> 10;
+  if (rounds > 0 && map != nullptr) {
+    h = run_rows<C, false>(map, lane0, 0, rounds, h, stage, bars, bars + C::STAGES, g, nullptr,
+                           nullptr);
+  } else if (threadIdx.x < C::LANES) {
+    for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
+  }
+  if (threadIdx.x >= C::LANES) return 0;
+  return tail_steps(h, p, nbytes, lane);
 }
 
 // depth-8 tree over 256 lanes in shared memory (pairs (2j, 2j+1), lower is a);
@@ -307,65 +308,108 @@ template <class C>
 __device__ __forceinline__ void init_bars(uint64_t *bars) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
-    if constexpr (C::PROD)
-      for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[C::STAGES + s], C::LANES / 32);
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[C::STAGES + s], C::WARPS);
     mbar_fence_init();
   }
   __syncthreads();
 }
 
-template <class C>
-__device__ __forceinline__ uint64_t hash_any(const uint8_t *p, uint64_t nbytes, const CUtensorMap *map,
-                                             uint32_t lane0, uint64_t h, uint8_t *stage, uint64_t *bars,
-                                             uint32_t &sync) {
-  if constexpr (C::PROD)
-    return hash_group_prod<C>(p, nbytes, map, lane0, h, stage, bars, bars + C::STAGES, sync);
-  else
-    return hash_group<C>(p, nbytes, map, lane0, h, stage, bars, sync);
+// Count one finished part; the CTA that completes all `parts` gets true.
+__device__ __forceinline__ bool last_part(uint32_t *counter, uint32_t parts, uint32_t *s_flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *s_flag = (atomicAdd(counter, 1u) == parts - 1) ? 1u : 0u;
+  __syncthreads();
+  const bool last = *s_flag != 0;
+  if (last) __threadfence();
+  return last;
 }
 
-// Work item = (entry, lane group); the last group of an entry folds.
+// Combine of the two-phase path: hi over the segments, the tail, the fold.
+__device__ __forceinline__ void big_combine(const HashEntry &E, uint64_t *lane_s) {
+  const uint64_t rounds = E.nbytes >> 10;
+  const uint32_t *lofinal = E.aux + (size_t)E.nseg * 256;
+  const uint32_t *A = lofinal + 256;
+  const uint32_t pw = pow435(kSegRows);
+  for (int lane = threadIdx.x; lane < 256; lane += blockDim.x) {
+    uint32_t hi = (uint32_t)(kFnvOffset >> 32);
+    for (uint32_t j = 0; j < E.nseg; ++j) {
+      const uint64_t m = min((uint64_t)kSegRows, rounds - (uint64_t)j * kSegRows);
+      hi = (m == kSegRows ? pw : pow435((uint32_t)m)) * hi + __ldcg(&A[(size_t)j * 256 + lane]);
+    }
+    const uint64_t h = ((uint64_t)hi << 32) | __ldcg(&lofinal[lane]);
+    lane_s[lane] = tail_steps(h, E.ptr, E.nbytes, lane);
+  }
+  const uint64_t root = tree_fold(lane_s);
+  if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+}
+
+// One launch for a batch of entries. Scratch: lanes[count x 256] (ordinary
+// entries' lane values), cnt = [count arrivals | item counter | nbig*G phase-1
+// progress counters | nbig completion counters].
 template <class C>
 __global__ void __launch_bounds__(C::THREADS)
-    simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *arrived) {
+    simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *cnt) {
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
   __shared__ uint64_t lane_s[256];
-  __shared__ uint32_t s_last;
+  __shared__ uint32_t s_flag, s_item;
   init_bars<C>(bars);
-  uint32_t parity = 0;
-  const uint32_t items = b.count * C::GROUPS;
-  // dynamic list scheduling: items are taken in LPT order (largest entries
-  // first) by whichever CTA is free, from a counter behind the arrival counts
-  uint32_t *next = arrived + b.count;
-  __shared__ uint32_t s_item;
-  for (uint32_t k = 0;; ++k) {
-    if (b.dynamic) {
-      if (threadIdx.x == 0) s_item = atomicAdd(next, 1u);
-      __syncthreads();
-    }
-    const uint32_t it = b.dynamic ? s_item : blockIdx.x + k * gridDim.x;
+  constexpr uint32_t G = C::GROUPS;
+  uint32_t *arrived = cnt;
+  uint32_t *next = cnt + b.count;
+  uint32_t *progress = next + 1;
+  uint32_t *bigdone = progress + b.nbig * G;
+  const uint32_t n1 = b.nbig * G, n2 = b.count * G, items = n2 + b.segmax * b.nbig * G;
+  uint32_t g = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1u);
+    __syncthreads();
+    const uint32_t it = s_item;
     if (it >= items) break;
-    const uint32_t e = it / C::GROUPS, g = it % C::GROUPS;
-    const HashEntry E = b.e[e];
-    const uint32_t lane0 = g * C::LANES;
-    uint64_t h = hash_any<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, parity);
-    if constexpr (C::GROUPS == 1) {
-      if (threadIdx.x < C::LANES) lane_s[threadIdx.x] = h;
-      uint64_t root = tree_fold(lane_s);
-      if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
-    } else {
+    if (it < n1) {
+      // phase 1: the lo chain of one lane group of a big entry
+      const uint32_t e = it / G, grp = it % G;
+      const HashEntry E = b.e[e];
+      const uint32_t lane0 = grp * C::LANES;
+      const uint64_t h = run_rows<C, true>(E.map, lane0, 0, E.nbytes >> 10, kFnvOffset, stage, bars,
+                                           bars + C::STAGES, g, E.aux, &progress[it]);
+      if (threadIdx.x < C::LANES) E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x] = (uint32_t)h;
+      if (last_part(&bigdone[e], G * (E.nseg + 1), &s_flag)) big_combine(E, lane_s);
+    } else if (it < n2) {
+      // an ordinary entry's lane group; the last group of the entry folds
+      const uint32_t e = it / G, grp = it % G;
+      const HashEntry E = b.e[e];
+      const uint32_t lane0 = grp * C::LANES;
+      const uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, g);
       if (threadIdx.x < C::LANES) lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) s_last = (atomicAdd(&arrived[e], 1u) == C::GROUPS - 1) ? 1u : 0u;
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
+      if (last_part(&arrived[e], G, &s_flag)) {
         for (int j = threadIdx.x; j < 256; j += blockDim.x)
           lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
-        uint64_t root = tree_fold(lane_s);
+        const uint64_t root = tree_fold(lane_s);
         if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+      }
+    } else {
+      // phase 2: segment j of one lane group of a big entry, once phase 1
+      // published the lo value that starts it
+      const uint32_t k = it - n2;
+      const uint32_t j = k / n1, r = k % n1, e = r / G, grp = r % G;
+      const HashEntry E = b.e[e];
+      if (j < E.nseg) {
+        if (threadIdx.x == 0)
+          while (ld_acquire(&progress[r]) < (j + 1) * C::WARPS) __nanosleep(256);
+        __syncthreads();
+        const uint32_t lane0 = grp * C::LANES;
+        const uint64_t rounds = E.nbytes >> 10;
+        const uint64_t row0 = (uint64_t)j * kSegRows;
+        const uint32_t lo0 =
+            threadIdx.x < C::LANES ? __ldcg(&E.aux[(size_t)j * 256 + lane0 + threadIdx.x]) : 0u;
+        const uint64_t h = run_rows<C, false>(E.map, lane0, row0, min((uint64_t)kSegRows, rounds - row0),
+                                              (uint64_t)lo0, stage, bars, bars + C::STAGES, g, nullptr,
+                                              nullptr);
+        if (threadIdx.x < C::LANES)
+          E.aux[(size_t)(E.nseg + 1) * 256 + (size_t)j * 256 + lane0 + threadIdx.x] = (uint32_t)(h >> 32);
+        if (last_part(&bigdone[e], G * (E.nseg + 1), &s_flag)) big_combine(E, lane_s);
       }
     }
     __syncthreads();
@@ -380,10 +424,10 @@ __global__ void __launch_bounds__(C::THREADS)
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
   init_bars<C>(bars);
-  uint32_t parity = 0;
+  uint32_t g = 0;
   const uint32_t lane = blockIdx.x * C::LANES + (threadIdx.x % C::LANES);
-  uint64_t h = hash_any<C>(p, nbytes, have_map ? &map : nullptr, blockIdx.x * C::LANES,
-                           state[lane], stage, bars, parity);
+  const uint64_t h = hash_group<C>(p, nbytes, have_map ? &map : nullptr, blockIdx.x * C::LANES,
+                                   state[lane], stage, bars, g);
   if (threadIdx.x < C::LANES) state[lane] = h;
 }
 
@@ -397,36 +441,13 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
-// Variants (env PCCLB_HASH_VARIANT, for experiments; 0 is the default),
-// measured on B200 with list scheduling (config-4 layout / one 1.05 GB entry /
-// 64 x 64 MiB, tools/hash_variants.py, median of 7):
-//   <128,128,3,P>  8.5 ms / 131 GB/s / 7.1 TB/s   (default)
-//   <64,128,4,P>   8.2 ms / 128 GB/s / 4.0 TB/s   (64 lanes per SM: HBM-starved)
-//   <128,64,3>    12.5 ms / 111 GB/s / 6.7 TB/s   (no producer warp; 10.6 ms grid-stride)
-//   <128,96,4,P>   9.0 ms / 123 GB/s / 7.1 TB/s
-// One entry is bounded by its lane chain (14.5 cycles per LOP3->IMAD.WIDE
-// step with the hi side interleaved, tools/micro/chain_lds.cu): 1 KiB per step
-// => 139 GB/s, 7.6 ms for the 1.05 GB embedding. Deep stages (128 rows) keep
-// ~2 us of TMA lookahead per CTA and amortise the per-stage handshakes.
-using HashV0 = HashCfg<128, 128, 3, true, true>;
-using HashV1 = HashCfg<64, 128, 4, true, true>;
-using HashV2 = HashCfg<128, 64, 3, true>;
-using HashV3 = HashCfg<128, 96, 4, true, true>;
-static bool hash_dynamic() {
+// PCCLB_HASH_TWO_PHASE=0 disables the two-phase path (measurements, tests)
+static bool two_phase_enabled() {
   static bool on = [] {
-    const char *e = getenv("PCCLB_HASH_DYN");
+    const char *e = getenv("PCCLB_HASH_TWO_PHASE");
     return !(e && e[0] == '0');
   }();
   return on;
-}
-
-int hash_variant() {
-  static int v = [] {
-    const char *e = getenv("PCCLB_HASH_VARIANT");
-    int x = e ? atoi(e) : 0;
-    return (x < 0 || x > 3) ? 0 : x;
-  }();
-  return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -447,7 +468,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // [rounds x 256] u32 view of an entry, box LANES x ROWS; false if not encodable
 template <class C>
 static bool encode_map(CUtensorMap *m, const void *p, uint64_t nbytes) {
-  const uint64_t rounds = (nbytes >> 2) >> 8;
+  const uint64_t rounds = nbytes >> 10;
   if (!rounds || (reinterpret_cast<uintptr_t>(p) & 15) || rounds >= (1ull << 31)) return false;
   auto fn = encode_fn();
   if (!fn) return false;
@@ -471,15 +492,6 @@ struct MapStaging {
   }
 };
 
-template <class C>
-static int prepare_variant() {
-  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_batch_kernel<C>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_update_kernel<C>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  return PCCLB_OK;
-}
-
 static int prepare_hash_kernels() {
   static std::mutex mu;
   static bool done[64] = {false};
@@ -487,18 +499,24 @@ static int prepare_hash_kernels() {
   PCCLB_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
   if (dev >= 0 && dev < 64 && done[dev]) return PCCLB_OK;
-  int rc = prepare_variant<HashV0>();
-  if (!rc) rc = prepare_variant<HashV1>();
-  if (!rc) rc = prepare_variant<HashV2>();
-  if (!rc) rc = prepare_variant<HashV3>();
-  if (rc) return rc;
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_batch_kernel<HashC>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, HashC::SMEM));
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_update_kernel<HashC>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, HashC::SMEM));
   if (dev >= 0 && dev < 64) done[dev] = true;
   return PCCLB_OK;
 }
 
-template <class C>
+// Big entries: those whose full-step chain (~139 GB/s) would outlast the
+// HBM-bound time of the whole call (total bytes at ~6 TB/s), at least 64 MiB.
+static bool is_big(uint64_t nbytes, uint64_t total) {
+  return two_phase_enabled() && nbytes >= (64ull << 20) && nbytes * 40 > total;
+}
+
+// order: entry indices, largest first
 static int launch_batches(const std::vector<uint32_t> &order, const void *const *h_ptrs,
                           const uint64_t *h_nbytes, uint64_t *d_out, cudaStream_t s) {
+  using C = HashC;
   const uint32_t count = (uint32_t)order.size();
   if (count == 0) return PCCLB_OK;
   int occ = 0;
@@ -506,56 +524,98 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
                                                            C::THREADS, C::SMEM));
   if (occ < 1) occ = 1;
   const uint32_t slots = (uint32_t)(sm_count() * occ);
-  // per-launch device scratch: lane values, arrival counters, tensor maps
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < count; ++i) total += h_nbytes[i];
+  // per-call device scratch: lane values, counters, tensor maps, big-entry aux
   const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
   const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  const size_t cnt_bytes = ((size_t)(m_max + 1) * sizeof(uint32_t) + 127) & ~size_t(127);
-  const size_t map_bytes = C::TMA2D ? (size_t)m_max * sizeof(CUtensorMap) : 0;
+  const size_t cnt_words = (size_t)m_max + 1 + kMaxBig * (C::GROUPS + 1);
+  const size_t cnt_bytes = (cnt_words * sizeof(uint32_t) + 127) & ~size_t(127);
+  const size_t map_bytes = (size_t)m_max * sizeof(CUtensorMap);
+  size_t aux_bytes = 0;
+  for (uint32_t i = 0, nb = 0; i < count && nb < kMaxBig; ++i) {
+    const uint64_t n = h_nbytes[order[i]];
+    if (!is_big(n, total)) continue;
+    const uint64_t nseg = ((n >> 10) + kSegRows - 1) / kSegRows;
+    aux_bytes += (2 * nseg + 1) * 256 * sizeof(uint32_t);
+    ++nb;
+  }
   char *scratch = nullptr;
-  PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), lanes_bytes + cnt_bytes + map_bytes, s));
+  PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch),
+                             lanes_bytes + cnt_bytes + map_bytes + aux_bytes, s));
   uint64_t *lanes = reinterpret_cast<uint64_t *>(scratch);
-  uint32_t *arrived = reinterpret_cast<uint32_t *>(scratch + lanes_bytes);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(scratch + lanes_bytes);
   CUtensorMap *d_maps = reinterpret_cast<CUtensorMap *>(scratch + lanes_bytes + cnt_bytes);
+  uint32_t *aux = reinterpret_cast<uint32_t *>(scratch + lanes_bytes + cnt_bytes + map_bytes);
   static thread_local HashBatch batch;
   static thread_local MapStaging staging;
   int rc = PCCLB_OK;
+  bool first = true;  // big entries are only taken in the first launch
   for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
     const uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
-    if (C::TMA2D) {
-      if (!staging.host) {
-        cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * kMaxBatch, cudaHostAllocDefault);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&staging.done, cudaEventDisableTiming);
-        if (e != cudaSuccess) {
-          rc = cuda_status(e);
-          break;
-        }
-      } else {
-        cudaEventSynchronize(staging.done);  // previous upload out of the staging area
+    if (!staging.host) {
+      cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * kMaxBatch, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&staging.done, cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        rc = cuda_status(e);
+        break;
       }
+    } else {
+      cudaEventSynchronize(staging.done);  // previous upload out of the staging area
     }
     batch.count = m;
-    batch.dynamic = hash_dynamic() ? 1u : 0u;
-    for (uint32_t i = 0; i < m; ++i) {
-      const uint32_t k = order[base + i];
-      HashEntry &E = batch.e[i];
+    batch.nbig = 0;
+    batch.segmax = 0;
+    uint32_t *aux_next = aux;
+    uint32_t slot = 0;
+    auto fill = [&](uint32_t k) {
+      HashEntry &E = batch.e[slot];
       E.ptr = static_cast<const uint8_t *>(h_ptrs[k]);
       E.nbytes = h_nbytes[k];
       E.out = d_out + k;
-      E.map = nullptr;
-      if (C::TMA2D && encode_map<C>(&staging.host[i], E.ptr, E.nbytes)) E.map = d_maps + i;
+      E.map = encode_map<C>(&staging.host[slot], E.ptr, E.nbytes) ? d_maps + slot : nullptr;
+      E.aux = nullptr;
+      E.nseg = 0;
+      E.pad = 0;
+      ++slot;
+      return E;
+    };
+    // big entries first (slots [0, nbig)), then the others in LPT order
+    std::vector<uint32_t> rest;
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint32_t k = order[base + i];
+      if (!(first && batch.nbig < kMaxBig && is_big(h_nbytes[k], total))) {
+        rest.push_back(k);
+        continue;
+      }
+      HashEntry &E = batch.e[slot];
+      fill(k);
+      if (!E.map) {  // no tensor map: ordinary entry after all
+        --slot;
+        rest.push_back(k);
+        continue;
+      }
+      E.nseg = (uint32_t)(((E.nbytes >> 10) + kSegRows - 1) / kSegRows);
+      E.aux = aux_next;
+      aux_next += (size_t)(2 * E.nseg + 1) * 256;
+      batch.segmax = std::max(batch.segmax, E.nseg);
+      ++batch.nbig;
     }
-    cudaError_t e = cudaSuccess;
-    if (C::TMA2D) {
-      e = cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
-      if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
-    }
-    if (e == cudaSuccess) e = cudaMemsetAsync(arrived, 0, (m + 1) * sizeof(uint32_t), s);
+    std::stable_sort(rest.begin(), rest.end(),
+                     [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
+    for (uint32_t k : rest) fill(k);
+    first = false;
+    cudaError_t e =
+        cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, cnt_words * sizeof(uint32_t), s);
     if (e != cudaSuccess) {
       rc = cuda_status(e);
       break;
     }
-    unsigned grid = std::min<uint32_t>(m * C::GROUPS, slots);
-    simplehash_batch_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(batch, lanes, arrived);
+    const uint64_t items = (uint64_t)m * C::GROUPS + (uint64_t)batch.segmax * batch.nbig * C::GROUPS;
+    const unsigned grid = (unsigned)std::min<uint64_t>(items, slots);
+    simplehash_batch_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(batch, lanes, cnt);
     e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_status(e);
   }
@@ -564,11 +624,11 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   return rc;
 }
 
-template <class C>
 static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaStream_t s) {
+  using C = HashC;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  int have = (C::TMA2D && encode_map<C>(&map, d, nbytes)) ? 1 : 0;
+  int have = encode_map<C>(&map, d, nbytes) ? 1 : 0;
   simplehash_update_kernel<C><<<C::GROUPS, C::THREADS, C::SMEM, s>>>(
       state, static_cast<const uint8_t *>(d), nbytes, map, have);
   PCCLB_LAUNCH_CHECK();
@@ -594,17 +654,7 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
   std::iota(order.begin(), order.end(), 0u);
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
-  cudaStream_t s = as_stream(stream);
-  switch (hash_variant()) {
-    case 1:
-      return launch_batches<HashV1>(order, h_ptrs, h_nbytes, d_out, s);
-    case 2:
-      return launch_batches<HashV2>(order, h_ptrs, h_nbytes, d_out, s);
-    case 3:
-      return launch_batches<HashV3>(order, h_ptrs, h_nbytes, d_out, s);
-    default:
-      return launch_batches<HashV0>(order, h_ptrs, h_nbytes, d_out, s);
-  }
+  return launch_batches(order, h_ptrs, h_nbytes, d_out, as_stream(stream));
 }
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {
@@ -623,7 +673,7 @@ int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uint64_t nbyt
   if (nbytes == 0) return PCCLB_OK;
   int rc = prepare_hash_kernels();
   if (rc) return rc;
-  return launch_update<HashV0>(d_state, d_data, nbytes, as_stream(stream));
+  return launch_update(d_state, d_data, nbytes, as_stream(stream));
 }
 
 int pcclb_simplehash_final(const uint64_t *d_state, uint64_t total_nbytes, uint64_t *d_out,

@@ -91,3 +91,37 @@ def test_one_bit_drift_detected():
     h0 = simplehash(x)
     x[123457] ^= 4
     assert simplehash(x) != h0
+
+
+@pytest.mark.parametrize("extra", [0, 1024 * 4096 - 1024, 3 * 1024 + 517, 1023, 1])
+def test_two_phase_big_entry_sizes(extra):
+    """Entries >= 64 MiB take the two-phase path (lo-chain checkpoints, segment
+    terms, combine): whole and partial last segments, tail words and bytes."""
+    from paper_2505_14065_b200 import simplehash
+
+    n = (64 << 20) + extra
+    raw = np.random.default_rng(extra).integers(0, 256, n, dtype=np.uint8)
+    assert simplehash(to_dev(raw)) == osh.simplehash_c(raw)
+
+
+def test_two_phase_mixed_batch():
+    """Two big entries beside many small ones in one launch (config-4 shape):
+    phase-2 segment items interleave with ordinary items."""
+    from paper_2505_14065_b200 import simplehash_many
+
+    rng = np.random.default_rng(77)
+    sizes = [(96 << 20) + 12345, (80 << 20) + 4096] + [int(x) for x in rng.integers(1, 1 << 20, 60)]
+    host = [rng.integers(0, 256, s, dtype=np.uint8) for s in sizes]
+    got = simplehash_many([to_dev(h) for h in host])
+    assert got == osh.simplehash_many_c(host, threads=8)
+
+
+def test_two_phase_repeated_calls_stable():
+    from paper_2505_14065_b200 import simplehash_many
+
+    x = torch.randint(0, 256, (200 << 20,), dtype=torch.uint8, device="cuda")
+    views = [x[: 150 << 20], x[150 << 20 :]]
+    first = simplehash_many(views)
+    for _ in range(3):
+        assert simplehash_many(views) == first
+    assert first[0] == osh.simplehash_c(views[0].cpu().numpy())
