@@ -26,9 +26,9 @@
 // splits into lo' = (lo ^ w) * 435 mod 2^32, which depends on lo alone, and
 // hi' = 435 hi + umulhi(x, 435) + (x << 8) with x = lo ^ w, which is affine in
 // hi. So:
-//   phase 1 (one item per lane group): run only the lo chain over the whole
-//     entry (10.5 instead of 14.5 cycles per step) and publish lo at every
-//     kSegRows-row checkpoint;
+//   phase 1 (one item per 64-lane quarter): run only the lo chain over the
+//     whole entry (10.5 instead of 14.5 cycles per step) and publish lo at
+//     every kSegRows-row checkpoint;
 //   phase 2 (one item per segment and lane group, run by any free CTA as soon
 //     as its checkpoint is published): rerun the full step over the segment
 //     from (lo = checkpoint, hi = 0), which leaves hi = A_j, the segment's
@@ -51,26 +51,37 @@
 
 namespace pcclb {
 
+// 12 resident CTAs' worth of registers (32 per thread): with more, ptxas
+// schedules the hi half of the full step worse (single 1 GB entry 11.2 vs
+// 8.1 ms measured with 48 registers)
+constexpr int kHashMinBlocks = 12;
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 constexpr uint32_t kSegRows = 4096;  // checkpoint spacing of the two-phase path (rows of 1 KiB)
 constexpr uint32_t kMaxBig = 16;     // big entries per launch
-constexpr int kMaxBatch = 640;       // HashBatch must fit the 32 KiB kernel-parameter space
+constexpr int kMaxBatch = 560;       // HashBatch must fit the 32 KiB kernel-parameter space
+// phase-1 items: 64 lanes per CTA and 256-row boxes, so each lo chain CTA keeps
+// ~2.7 us of TMA in flight (the lo chain consumes 512 B per ~10.5 cycles per
+// 128 lanes, more than one CTA's stream of 128-lane boxes sustains)
+constexpr int kP1Lanes = 64;
+constexpr int kP1Rows = 256;
+constexpr int kP1Groups = 256 / kP1Lanes;
 
 struct HashEntry {
   const uint8_t *ptr;
   uint64_t nbytes;
   uint64_t *out;
   const CUtensorMap *map;  // 2-D view [rounds x 256] u32, or null (direct loads)
+  const CUtensorMap *map1; // big entries: the same view with phase-1 boxes
   uint32_t *aux;           // big entries: [nseg x 256] checkpoints, [256] final lo, [nseg x 256] A
   uint32_t nseg;           // big entries: number of kSegRows segments
   uint32_t pad;
 };
 
 // Entries [0, nbig) are big (two-phase); item space:
-//   [0, nbig*G)                         phase-1 lo chains
-//   [nbig*G, count*G)                   ordinary entries
-//   [count*G, count*G + segmax*nbig*G)  phase-2 segments, segment-major
+//   [0, n1 = nbig*P1)                   phase-1 lo chains (P1 = kP1Groups)
+//   [n1, n2 = n1 + (count-nbig)*G)      ordinary entries' lane groups
+//   [n2, n2 + segmax*nbig*G)            phase-2 segments, segment-major
 struct HashBatch {
   uint32_t count;
   uint32_t nbig;
@@ -186,20 +197,22 @@ struct HashCfg {
 // stages keep ~2 us of TMA lookahead per CTA and amortise the handshakes.
 using HashC = HashCfg<128, 128, 3>;
 
-// Rows [row0, row0 + nrows) of lanes [lane0, lane0 + LANES) through the TMA
-// ring; h is the lane's state (lane threads). The producer thread (thread
-// LANES) issues a stage into slot g % STAGES once the lane warps released it
-// (empty[slot], one arrival per lane warp); `g` numbers the stages of the whole
-// launch, so the mbarrier phase parity is (g / STAGES) & 1. LO_ONLY: step the
-// lo chain only and, every kSegRows rows (row0 = 0), store the lo value that
-// starts the segment to ck[seg * 256 + lane] and count it in *progress.
-template <class C, bool LO_ONLY>
+// Rows [row0, row0 + nrows) of lanes [lane0, lane0 + L) through the TMA ring
+// (boxes of L lanes x R rows); h is the lane's state (threads < L). The
+// producer thread (thread C::LANES) issues a stage into slot g % STAGES once
+// the C::WARPS lane warps released it (empty[slot]); `g` numbers the stages of
+// the whole launch, so the mbarrier phase parity is (g / STAGES) & 1. Lane
+// warps beyond L only keep the ring protocol. LO_ONLY: step the lo chain only
+// and, every kSegRows rows (row0 = 0), store the lo value that starts the
+// segment to ck[seg * 256 + lane] and count each writing warp in *progress.
+template <class C, int L, int R, bool LO_ONLY>
 __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t lane0, uint64_t row0,
                                              uint64_t nrows, uint64_t h, uint8_t *stage,
                                              uint64_t *full, uint64_t *empty, uint32_t &g,
                                              uint32_t *ck, uint32_t *progress) {
+  static_assert(L * R * 4 <= C::STAGE_BYTES && L <= C::LANES && kSegRows % R == 0, "box fits a slot");
   const int tid = threadIdx.x;
-  const uint32_t nst = (uint32_t)((nrows + C::ROWS - 1) / C::ROWS);
+  const uint32_t nst = (uint32_t)((nrows + R - 1) / R);
   if (tid >= C::LANES) {
     if (tid == C::LANES) {
       tensormap_acquire(map);
@@ -207,50 +220,56 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
         const uint32_t G = g + s, slot = G % C::STAGES;
         if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
         // rows past the end of the tensor are zero-filled and still counted
-        mbar_expect_tx(&full[slot], C::STAGE_BYTES);
-        tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(row0 + (uint64_t)s * C::ROWS),
+        mbar_expect_tx(&full[slot], L * R * 4);
+        tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(row0 + (uint64_t)s * R),
                    &full[slot]);
       }
     }
   } else {
-    Fnv f(h);
+    const bool active = tid < L;
     for (uint32_t s = 0; s < nst; ++s) {
       const uint32_t G = g + s, slot = G % C::STAGES;
       if constexpr (LO_ONLY) {
-        if ((s * C::ROWS) % kSegRows == 0) {
-          ck[(s * C::ROWS / kSegRows) * 256 + lane0 + tid] = f.lo;
+        if (active && (s * R) % kSegRows == 0) {
+          ck[(s * R / kSegRows) * 256 + lane0 + tid] = (uint32_t)h;
           __syncwarp();
           if ((tid & 31) == 0) {
-            __threadfence();
+            __threadfence();  // ~3% of phase 1 (measured against an unordered count)
             atomicAdd(progress, 1u);
           }
         }
       }
       mbar_wait(&full[slot], (G / C::STAGES) & 1u);
-      const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
-      const uint64_t left = nrows - (uint64_t)s * C::ROWS;
-      if (left >= (uint64_t)C::ROWS) {
-        // fully unrolled: the shared-memory loads are hoisted ahead of the chain
+      if (active) {
+        // the state is unpacked per stage: it keeps the compiler from
+        // rescheduling the hi chain across stages (measured 35% slower)
+        Fnv f(h);
+        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
+        const uint64_t left = nrows - (uint64_t)s * R;
+        if (left >= (uint64_t)R) {
+          // fully unrolled: the shared-memory loads are hoisted ahead of the chain
+          // (measured best for both forms, e.g. phase 1: 6.24 ms at 256 vs 6.8 at 32)
 #pragma unroll
-        for (int r = 0; r < C::ROWS; ++r) {
-          if constexpr (LO_ONLY)
-            f.step_lo(wds[r * C::LANES]);
-          else
-            f.step(wds[r * C::LANES]);
+          for (int r = 0; r < R; ++r) {
+            if constexpr (LO_ONLY)
+              f.step_lo(wds[r * L]);
+            else
+              f.step(wds[r * L]);
+          }
+        } else {
+          const int nr = (int)left;
+          for (int r = 0; r < nr; ++r) {
+            if constexpr (LO_ONLY)
+              f.step_lo(wds[r * L]);
+            else
+              f.step(wds[r * L]);
+          }
         }
-      } else {
-        const int nr = (int)left;
-        for (int r = 0; r < nr; ++r) {
-          if constexpr (LO_ONLY)
-            f.step_lo(wds[r * C::LANES]);
-          else
-            f.step(wds[r * C::LANES]);
-        }
+        h = f.value();
       }
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
     }
-    h = f.value();
   }
   g += nst;
   return h;
@@ -278,8 +297,8 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
   const uint32_t lane = lane0 + threadIdx.x;
   const uint64_t rounds = nbytes >> 10;
   if (rounds > 0 && map != nullptr) {
-    h = run_rows<C, false>(map, lane0, 0, rounds, h, stage, bars, bars + C::STAGES, g, nullptr,
-                           nullptr);
+    h = run_rows<C, C::LANES, C::ROWS, false>(map, lane0, 0, rounds, h, stage, bars, bars + C::STAGES, g,
+                                              nullptr, nullptr);
   } else if (threadIdx.x < C::LANES) {
     for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
   }
@@ -333,6 +352,7 @@ __device__ __forceinline__ void big_combine(const HashEntry &E, uint64_t *lane_s
   const uint32_t pw = pow435(kSegRows);
   for (int lane = threadIdx.x; lane < 256; lane += blockDim.x) {
     uint32_t hi = (uint32_t)(kFnvOffset >> 32);
+#pragma unroll 8
     for (uint32_t j = 0; j < E.nseg; ++j) {
       const uint64_t m = min((uint64_t)kSegRows, rounds - (uint64_t)j * kSegRows);
       hi = (m == kSegRows ? pw : pow435((uint32_t)m)) * hi + __ldcg(&A[(size_t)j * 256 + lane]);
@@ -348,19 +368,20 @@ __device__ __forceinline__ void big_combine(const HashEntry &E, uint64_t *lane_s
 // entries' lane values), cnt = [count arrivals | item counter | nbig*G phase-1
 // progress counters | nbig completion counters].
 template <class C>
-__global__ void __launch_bounds__(C::THREADS)
+__global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
     simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *cnt) {
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
   __shared__ uint64_t lane_s[256];
   __shared__ uint32_t s_flag, s_item;
   init_bars<C>(bars);
-  constexpr uint32_t G = C::GROUPS;
+  constexpr uint32_t G = C::GROUPS, P1 = kP1Groups;
   uint32_t *arrived = cnt;
   uint32_t *next = cnt + b.count;
   uint32_t *progress = next + 1;
-  uint32_t *bigdone = progress + b.nbig * G;
-  const uint32_t n1 = b.nbig * G, n2 = b.count * G, items = n2 + b.segmax * b.nbig * G;
+  uint32_t *bigdone = progress + b.nbig * P1;
+  const uint32_t n1 = b.nbig * P1, n2 = n1 + (b.count - b.nbig) * G, nseg_items = b.nbig * G;
+  const uint32_t items = n2 + b.segmax * nseg_items;
   uint32_t g = 0;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(next, 1u);
@@ -368,17 +389,18 @@ __global__ void __launch_bounds__(C::THREADS)
     const uint32_t it = s_item;
     if (it >= items) break;
     if (it < n1) {
-      // phase 1: the lo chain of one lane group of a big entry
-      const uint32_t e = it / G, grp = it % G;
+      // phase 1: the lo chain of one 64-lane quarter of a big entry
+      const uint32_t e = it / P1, q = it % P1;
       const HashEntry E = b.e[e];
-      const uint32_t lane0 = grp * C::LANES;
-      const uint64_t h = run_rows<C, true>(E.map, lane0, 0, E.nbytes >> 10, kFnvOffset, stage, bars,
-                                           bars + C::STAGES, g, E.aux, &progress[it]);
-      if (threadIdx.x < C::LANES) E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x] = (uint32_t)h;
-      if (last_part(&bigdone[e], G * (E.nseg + 1), &s_flag)) big_combine(E, lane_s);
+      const uint32_t lane0 = q * kP1Lanes;
+      const uint64_t h = run_rows<C, kP1Lanes, kP1Rows, true>(E.map1, lane0, 0, E.nbytes >> 10, kFnvOffset,
+                                                              stage, bars, bars + C::STAGES, g, E.aux,
+                                                              &progress[it]);
+      if (threadIdx.x < kP1Lanes) E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x] = (uint32_t)h;
+      if (last_part(&bigdone[e], P1 + G * E.nseg, &s_flag)) big_combine(E, lane_s);
     } else if (it < n2) {
       // an ordinary entry's lane group; the last group of the entry folds
-      const uint32_t e = it / G, grp = it % G;
+      const uint32_t e = b.nbig + (it - n1) / G, grp = (it - n1) % G;
       const HashEntry E = b.e[e];
       const uint32_t lane0 = grp * C::LANES;
       const uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, g);
@@ -390,26 +412,29 @@ __global__ void __launch_bounds__(C::THREADS)
         if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
       }
     } else {
-      // phase 2: segment j of one lane group of a big entry, once phase 1
-      // published the lo value that starts it
-      const uint32_t k = it - n2;
-      const uint32_t j = k / n1, r = k % n1, e = r / G, grp = r % G;
+      // phase 2: segment j of one 128-lane group of a big entry, once phase 1
+      // published the lo values that start it (two 64-lane quarters)
+      const uint32_t kk = it - n2;
+      const uint32_t j = kk / nseg_items, r = kk % nseg_items, e = r / G, grp = r % G;
       const HashEntry E = b.e[e];
       if (j < E.nseg) {
-        if (threadIdx.x == 0)
-          while (ld_acquire(&progress[r]) < (j + 1) * C::WARPS) __nanosleep(256);
+        if (threadIdx.x == 0) {
+          constexpr uint32_t per = C::LANES / kP1Lanes, wq = kP1Lanes / 32;
+          for (uint32_t q = 0; q < per; ++q)
+            while (ld_acquire(&progress[e * P1 + grp * per + q]) < (j + 1) * wq) __nanosleep(256);
+        }
         __syncthreads();
         const uint32_t lane0 = grp * C::LANES;
         const uint64_t rounds = E.nbytes >> 10;
         const uint64_t row0 = (uint64_t)j * kSegRows;
         const uint32_t lo0 =
             threadIdx.x < C::LANES ? __ldcg(&E.aux[(size_t)j * 256 + lane0 + threadIdx.x]) : 0u;
-        const uint64_t h = run_rows<C, false>(E.map, lane0, row0, min((uint64_t)kSegRows, rounds - row0),
-                                              (uint64_t)lo0, stage, bars, bars + C::STAGES, g, nullptr,
-                                              nullptr);
+        const uint64_t h = run_rows<C, C::LANES, C::ROWS, false>(
+            E.map, lane0, row0, min((uint64_t)kSegRows, rounds - row0), (uint64_t)lo0, stage, bars,
+            bars + C::STAGES, g, nullptr, nullptr);
         if (threadIdx.x < C::LANES)
           E.aux[(size_t)(E.nseg + 1) * 256 + (size_t)j * 256 + lane0 + threadIdx.x] = (uint32_t)(h >> 32);
-        if (last_part(&bigdone[e], G * (E.nseg + 1), &s_flag)) big_combine(E, lane_s);
+        if (last_part(&bigdone[e], P1 + G * E.nseg, &s_flag)) big_combine(E, lane_s);
       }
     }
     __syncthreads();
@@ -465,8 +490,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// [rounds x 256] u32 view of an entry, box LANES x ROWS; false if not encodable
-template <class C>
+// [rounds x 256] u32 view of an entry, box L lanes x R rows; false if not encodable
+template <int L, int R>
 static bool encode_map(CUtensorMap *m, const void *p, uint64_t nbytes) {
   const uint64_t rounds = nbytes >> 10;
   if (!rounds || (reinterpret_cast<uintptr_t>(p) & 15) || rounds >= (1ull << 31)) return false;
@@ -474,7 +499,7 @@ static bool encode_map(CUtensorMap *m, const void *p, uint64_t nbytes) {
   if (!fn) return false;
   cuuint64_t dims[2] = {256, rounds};
   cuuint64_t strides[1] = {1024};
-  cuuint32_t box[2] = {(cuuint32_t)C::LANES, (cuuint32_t)C::ROWS};
+  cuuint32_t box[2] = {(cuuint32_t)L, (cuuint32_t)R};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(p), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -529,9 +554,9 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   // per-call device scratch: lane values, counters, tensor maps, big-entry aux
   const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
   const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  const size_t cnt_words = (size_t)m_max + 1 + kMaxBig * (C::GROUPS + 1);
+  const size_t cnt_words = (size_t)m_max + 1 + kMaxBig * (kP1Groups + 1);
   const size_t cnt_bytes = (cnt_words * sizeof(uint32_t) + 127) & ~size_t(127);
-  const size_t map_bytes = (size_t)m_max * sizeof(CUtensorMap);
+  const size_t map_bytes = ((size_t)kMaxBatch + kMaxBig) * sizeof(CUtensorMap);
   size_t aux_bytes = 0;
   for (uint32_t i = 0, nb = 0; i < count && nb < kMaxBig; ++i) {
     const uint64_t n = h_nbytes[order[i]];
@@ -554,7 +579,8 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
     const uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
     if (!staging.host) {
-      cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * kMaxBatch, cudaHostAllocDefault);
+      cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * (kMaxBatch + kMaxBig),
+                                    cudaHostAllocDefault);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&staging.done, cudaEventDisableTiming);
       if (e != cudaSuccess) {
         rc = cuda_status(e);
@@ -573,7 +599,8 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       E.ptr = static_cast<const uint8_t *>(h_ptrs[k]);
       E.nbytes = h_nbytes[k];
       E.out = d_out + k;
-      E.map = encode_map<C>(&staging.host[slot], E.ptr, E.nbytes) ? d_maps + slot : nullptr;
+      E.map = encode_map<C::LANES, C::ROWS>(&staging.host[slot], E.ptr, E.nbytes) ? d_maps + slot : nullptr;
+      E.map1 = nullptr;
       E.aux = nullptr;
       E.nseg = 0;
       E.pad = 0;
@@ -590,11 +617,13 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       }
       HashEntry &E = batch.e[slot];
       fill(k);
-      if (!E.map) {  // no tensor map: ordinary entry after all
-        --slot;
+      const uint32_t mi = kMaxBatch + batch.nbig;  // phase-1 map slot
+      if (!E.map || !encode_map<kP1Lanes, kP1Rows>(&staging.host[mi], E.ptr, E.nbytes)) {
+        --slot;  // no tensor map: ordinary entry after all
         rest.push_back(k);
         continue;
       }
+      E.map1 = d_maps + mi;
       E.nseg = (uint32_t)(((E.nbytes >> 10) + kSegRows - 1) / kSegRows);
       E.aux = aux_next;
       aux_next += (size_t)(2 * E.nseg + 1) * 256;
@@ -607,13 +636,17 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
     first = false;
     cudaError_t e =
         cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && batch.nbig)
+      e = cudaMemcpyAsync(d_maps + kMaxBatch, staging.host + kMaxBatch, sizeof(CUtensorMap) * batch.nbig,
+                          cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, cnt_words * sizeof(uint32_t), s);
     if (e != cudaSuccess) {
       rc = cuda_status(e);
       break;
     }
-    const uint64_t items = (uint64_t)m * C::GROUPS + (uint64_t)batch.segmax * batch.nbig * C::GROUPS;
+    const uint64_t items = (uint64_t)batch.nbig * kP1Groups + (uint64_t)(m - batch.nbig) * C::GROUPS +
+                           (uint64_t)batch.segmax * batch.nbig * C::GROUPS;
     const unsigned grid = (unsigned)std::min<uint64_t>(items, slots);
     simplehash_batch_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(batch, lanes, cnt);
     e = cudaGetLastError();
@@ -628,7 +661,7 @@ static int launch_update(uint64_t *state, const void *d, uint64_t nbytes, cudaSt
   using C = HashC;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  int have = encode_map<C>(&map, d, nbytes) ? 1 : 0;
+  int have = encode_map<C::LANES, C::ROWS>(&map, d, nbytes) ? 1 : 0;
   simplehash_update_kernel<C><<<C::GROUPS, C::THREADS, C::SMEM, s>>>(
       state, static_cast<const uint8_t *>(d), nbytes, map, have);
   PCCLB_LAUNCH_CHECK();

@@ -53,4 +53,13 @@ res["single_1GB"], _ = timeit([views[0]], 5)
 eq = state[: 64 * (32 << 20)].view(64, -1)
 res["64x64MiB"], _ = timeit([eq[i] for i in range(64)], 7)
 res["digest0"] = digests[0] & 0xFFFFFFFFFFFFFFFF
-print(json.dumps(res))
+print(json.dumps(res), flush=True)
+try:
+    import pynvml
+
+    pynvml.nvmlInit()
+    hd = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    print(json.dumps({"sm_mhz_after": pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM),
+                      "reasons": int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(hd))}))
+except Exception as exc:  # noqa: BLE001
+    print(json.dumps({"nvml": str(exc)}))

@@ -175,11 +175,14 @@ int main() {
       printf("tma2d box=%3dx%3d nst=%d ctas=%4d : %8.1f GB/s total, %7.1f GB/s per CTA (%s)\n", boxw, boxh, nst, ctas,
              bytes / ms / 1e6, bytes / ms / 1e6 / ctas, cudaGetErrorString(cudaGetLastError()));
     };
-    for (int ctas : {1, 2, 4, 296}) {
-      run2d(tma2d_stream<128, 64, 3>, 128, 64, 3, ctas);
+    for (int ctas : {1, 4}) {
+      run2d(tma2d_stream<64, 256, 3>, 64, 256, 3, ctas);
+      run2d(tma2d_stream<64, 128, 6>, 64, 128, 6, ctas);
+      run2d(tma2d_stream<128, 128, 3>, 128, 128, 3, ctas);
       run2d(tma2d_stream<128, 64, 6>, 128, 64, 6, ctas);
+      run2d(tma2d_stream<256, 64, 3>, 256, 64, 3, ctas);
       run2d(tma2d_stream<256, 32, 6>, 256, 32, 6, ctas);
-      run2d(tma2d_stream<64, 128, 4>, 64, 128, 4, ctas);
+      run2d(tma2d_stream<256, 16, 12>, 256, 16, 12, ctas);
     }
   }
   uint64_t *out; long long *cyc; long long h;
