@@ -245,6 +245,8 @@ def bench_hash(args, rank, world, local):
 
     pk = peaks()
     achieved = nbytes / (ms * 1e-3) / 1e9
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965
+    chain_floor_ms = (views[0].numel() * 2 // 1024) * 10.5 / (sm_mhz * 1e6) * 1e3
     result = {
         "value": round(world * nbytes / (ms_max * 1e-3) / 1e9, 2),
         "unit": "GB/s",
@@ -258,7 +260,12 @@ def bench_hash(args, rank, world, local):
                      "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
                      "kernel": "simplehash_batch_kernel", "algorithmic_bytes_per_launch": nbytes,
                      "largest_entry_alone_ms": round(big_ms, 3),
-                     "largest_entry_alone_gbs": round(views[0].numel() * 2 / (big_ms * 1e-3) / 1e9, 1)},
+                     "largest_entry_alone_gbs": round(views[0].numel() * 2 / (big_ms * 1e-3) / 1e9, 1),
+                     # the largest entry's 256 lanes are serial chains: even the lo-chain
+                     # phase needs 10.5 cycles per 1 KiB row (tools/micro/chain_lds.cu)
+                     "latency_floor_ms": round(chain_floor_ms, 3),
+                     "frac_of_latency_floor": round(chain_floor_ms / ms, 4),
+                     "hbm_floor_ms": round(nbytes / (pk["hbm_gbs"] * 1e9) * 1e3, 3)},
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches,
