@@ -210,7 +210,8 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
                                              uint64_t nrows, uint64_t h, uint8_t *stage,
                                              uint64_t *full, uint64_t *empty, uint32_t &g,
                                              uint32_t *ck, uint32_t *progress) {
-  static_assert(L * R * 4 <= C::STAGE_BYTES && L <= C::LANES && kSegRows % R == 0, "box fits a slot");
+  static_assert(L * R * 4 <= C::STAGE_BYTES && kSegRows % R == 0, "box fits a slot");
+  static_assert(L == C::LANES || L + 32 <= C::LANES, "narrow boxes start at warp 1");
   const int tid = threadIdx.x;
   const uint32_t nst = (uint32_t)((nrows + R - 1) / R);
   if (tid >= C::LANES) {
@@ -226,12 +227,15 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
       }
     }
   } else {
-    const bool active = tid < L;
+    // narrower boxes run on warps 1.. (warp 0 shares its SMSP with the producer)
+    constexpr int off = (L < C::LANES) ? 32 : 0;
+    const int t = tid - off;
+    const bool active = t >= 0 && t < L;
     for (uint32_t s = 0; s < nst; ++s) {
       const uint32_t G = g + s, slot = G % C::STAGES;
       if constexpr (LO_ONLY) {
         if (active && (s * R) % kSegRows == 0) {
-          ck[(s * R / kSegRows) * 256 + lane0 + tid] = (uint32_t)h;
+          ck[(s * R / kSegRows) * 256 + lane0 + t] = (uint32_t)h;
           __syncwarp();
           if ((tid & 31) == 0) {
             __threadfence();  // ~3% of phase 1 (measured against an unordered count)
@@ -244,7 +248,7 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
         // the state is unpacked per stage: it keeps the compiler from
         // rescheduling the hi chain across stages (measured 35% slower)
         Fnv f(h);
-        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + tid;
+        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + t;
         const uint64_t left = nrows - (uint64_t)s * R;
         if (left >= (uint64_t)R) {
           // fully unrolled: the shared-memory loads are hoisted ahead of the chain
@@ -396,7 +400,8 @@ __global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
       const uint64_t h = run_rows<C, kP1Lanes, kP1Rows, true>(E.map1, lane0, 0, E.nbytes >> 10, kFnvOffset,
                                                               stage, bars, bars + C::STAGES, g, E.aux,
                                                               &progress[it]);
-      if (threadIdx.x < kP1Lanes) E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x] = (uint32_t)h;
+      if (threadIdx.x >= 32 && threadIdx.x < 32 + kP1Lanes)  // run_rows' lane offset
+        E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x - 32] = (uint32_t)h;
       if (last_part(&bigdone[e], P1 + G * E.nseg, &s_flag)) big_combine(E, lane_s);
     } else if (it < n2) {
       // an ordinary entry's lane group; the last group of the entry folds
