@@ -310,7 +310,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     src = torch.randn(n, generator=g, device=dev) * (1e-2 if quantize else 1.0)
     buf = torch.empty_like(src)
     esz = 4
-    ring = DeviceRing(device=dev, capacity_bytes=16384 + n * esz + 4 * (n // world + 1) * esz + (1 << 20))
+    ring = DeviceRing(device=dev, capacity_bytes=DeviceRing.required_bytes(n, world, esz, quantize))
     if not args.no_register:
         ring.register(buf)  # one-time collective setup: peers read buf in place (zero-copy)
     stream = torch.cuda.current_stream(dev)

@@ -182,6 +182,12 @@ PCCLB_API int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle
 /* Host-mapped abort word the control plane may set (reference: the tag box
  * abort_event set on ABORT_NOTIFY, client.py:196-204). Returns host pointer. */
 PCCLB_API volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r);
+/* Number of engines that may run ops concurrently on this GPU (the
+ * communicator's pool of slots, client.py:482-486; default 2). The fused
+ * quantized steps spin on peer-ready flags with persistent CTAs, so each engine
+ * takes at most its share of the SM's CTA slots; with more engines than slots
+ * the engine falls back to one barrier per ring step. */
+PCCLB_API int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots);
 /* Element capacity for a dtype/quantize combination with this workspace. */
 PCCLB_API uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize);
 

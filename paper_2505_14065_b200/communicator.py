@@ -131,7 +131,8 @@ class Communicator:
         self.group = group
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.pool_size = pool_size
-        self.engines = [DeviceRing(group, ring, self.device, capacity_bytes, timeout_s) for _ in range(pool_size)]
+        self.engines = [DeviceRing(group, ring, self.device, capacity_bytes, timeout_s, slots=pool_size)
+                        for _ in range(pool_size)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(pool_size)]
         self._handles: dict[int, AsyncHandle] = {}
         self.stats = {"reduce_attempts": 0, "reduce_completed": 0, "reduce_aborted": 0, "sync_calls": 0,

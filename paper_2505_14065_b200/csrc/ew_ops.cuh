@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t code_byte(const uint4 &q, int k) {
   return (w >> (8 * (k & 3))) & 0xffu;
 }
 
-template <int OP>
+template <int OP, bool X86 = true>
 struct DequantAcc16F {
   float *__restrict__ acc;
   const uint8_t *__restrict__ codes;
@@ -170,14 +170,15 @@ struct DequantAcc16F {
   RangeAcc r;
   float *__restrict__ bak;  // nullable: save acc's old value first
   __device__ __forceinline__ float step(float local, uint32_t q) {
-    float v = reduce_op<OP>(local, dequant1(q, mn, scale));
+    float v = reduce_op_x<OP, X86>(local, dequant1x<X86>(q, mn, scale));
     r.add(v);
     return v;
   }
+  // codes are read with ld.global.cg (L2): a peer wrote them during this op
   __device__ __forceinline__ void one(uint64_t i) {
     const float old = acc[i];
     if (bak) bak[i] = old;
-    acc[i] = step(old, codes[i]);
+    acc[i] = step(old, __ldcg(codes + i));
   }
   struct In {
     Pack16<float> a[4];
@@ -185,7 +186,7 @@ struct DequantAcc16F {
   };
   __device__ __forceinline__ In vload(uint64_t i) {
     In v;
-    v.q = *reinterpret_cast<const uint4 *>(codes + i);
+    v.q = __ldcg(reinterpret_cast<const uint4 *>(codes + i));
 #pragma unroll
     for (int g = 0; g < 4; ++g) v.a[g] = ld16(acc + i + 4 * g);
     return v;
@@ -202,18 +203,19 @@ struct DequantAcc16F {
   }
 };
 
-struct Dequant16F {
+template <bool X86>
+struct Dequant16T {
   float *__restrict__ out;
   const uint8_t *__restrict__ codes;
   float mn, scale, avg;
   bool do_div;
   __device__ __forceinline__ float val(uint32_t q) {
-    float d = dequant1(q, mn, scale);
-    return do_div ? div_world(d, avg) : d;
+    float d = dequant1x<X86>(q, mn, scale);
+    return do_div ? div_world_x<X86>(d, avg) : d;
   }
-  __device__ __forceinline__ void one(uint64_t i) { out[i] = val(codes[i]); }
+  __device__ __forceinline__ void one(uint64_t i) { out[i] = val(__ldcg(codes + i)); }
   using In = uint4;
-  __device__ __forceinline__ In vload(uint64_t i) { return *reinterpret_cast<const uint4 *>(codes + i); }
+  __device__ __forceinline__ In vload(uint64_t i) { return __ldcg(reinterpret_cast<const uint4 *>(codes + i)); }
   __device__ __forceinline__ void vapply(uint64_t i, const In &q) {
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -224,6 +226,8 @@ struct Dequant16F {
     }
   }
 };
+
+using Dequant16F = Dequant16T<true>;
 
 struct Quant16F {
   const float *__restrict__ x;

@@ -168,9 +168,10 @@ __device__ __forceinline__ QParams qparams_from_range(const pcclb_range &r) {
   return q;
 }
 
-// q = u8(clip(rint((x - min) / scale), 0, 255)); NaN -> 0
+// q = u8(clip(rint((x - min) / scale), 0, 255)); NaN -> 0. A NaN's payload
+// never reaches the code, so plain IEEE operations give the reference's codes.
 __device__ __forceinline__ uint32_t quant1(float x, float mn, float scale) {
-  float t = x86_div(x86_sub(x, mn), scale);
+  float t = __fdiv_rn(__fsub_rn(x, mn), scale);
   t = rintf(t);
   if (is_nan(t)) return 0u;
   t = fminf(fmaxf(t, 0.0f), 255.0f);
@@ -189,7 +190,7 @@ static __device__ __noinline__ uint32_t quant1_exact(float x, float mn, float sc
 // (relative) of 0.5, where the exact division decides. Non-finite t (d or
 // 1/scale overflowing) also takes the exact path.
 __device__ __forceinline__ uint32_t quant1_fast(float x, float mn, float scale, float inv) {
-  const float d = x86_sub(x, mn);
+  const float d = __fsub_rn(x, mn);
   const float t = __fmul_rn(d, inv);
   const float fl = floorf(t);
   const float h = __fsub_rn(t, fl);            // exact for t < 2^23
@@ -205,6 +206,30 @@ __device__ __forceinline__ uint32_t quant1_fast(float x, float mn, float scale, 
 // x = f32(q) * scale (RN) + min (RN), x86 NaN rules
 __device__ __forceinline__ float dequant1(uint32_t q, float mn, float scale) {
   return x86_add(x86_mul((float)q, scale), mn);
+}
+// X86 = false: plain IEEE operations, for kernels where a NaN cannot occur
+// (finite scale and min) or can only occur in an op that is then aborted and
+// restored (any NaN in a partial sum makes the next range non-finite), so
+// the x86 payload rules cannot change a delivered result
+template <bool X86>
+__device__ __forceinline__ float dequant1x(uint32_t q, float mn, float scale) {
+  if constexpr (X86) return dequant1(q, mn, scale);
+  else return __fadd_rn(__fmul_rn((float)q, scale), mn);
+}
+template <bool X86>
+__device__ __forceinline__ float div_world_x(float x, float w) {
+  if constexpr (X86) {
+    return div_world(x, w);
+  } else {
+    const uint32_t b = __float_as_uint(w);
+    if ((b & 0x007fffffu) == 0u) return __fmul_rn(x, __uint_as_float((254u << 23) - b));
+    return __fdiv_rn(x, w);
+  }
+}
+template <int OP, bool X86, typename T>
+__device__ __forceinline__ T reduce_op_x(T local, T incoming) {
+  if constexpr (X86 || OP == PCCLB_MAX || OP == PCCLB_MIN) return reduce_op<OP>(local, incoming);
+  else return FTraits<T>::add(local, incoming);
 }
 
 // block-wide range accumulation helpers

@@ -13,8 +13,11 @@
 //                     quantization metas, range slots, status word
 //   in   [N elems]    copy of the caller's input = the backup (collective.py:501-504)
 //   res  [n_c elems]  plain: fold result of the owned chunk
-//   codes0/1 [n_c B]  quantized: wire codes of reduce steps (double-buffered)
+//   codes[s] [n_c B]  quantized: wire codes of reduce step s, written by the
+//                     predecessor (one buffer per step: no reuse within an op)
 //   codesF   [n_c B]  quantized: owned chunk's final codes for the gather
+//   flags[s] [u64 per 64 Ki-element block] quantized: block-ready tokens of
+//                     step s, written by the predecessor
 //
 // Plain schedule (2 barriers). Each chunk's fold chain x_c, x_{c+1}, ..., x_{c-1}
 // (SURVEY §0 finding 2) is computed by the chunk's owner (rank c-1, as in the
@@ -69,6 +72,8 @@ namespace pcclb {
 constexpr int kIpcMaxWorld = 64;
 constexpr uint64_t kSignalBytes = 16384;
 constexpr int kIpcThreads = 512;
+constexpr uint64_t kQB = 65536;  // elements per ready-flag block of the fused quantized steps
+constexpr int kQThreads = 256;
 
 struct Signal {
   uint64_t arrive[kIpcMaxWorld];     // written by peer j: its latest barrier token
@@ -79,6 +84,9 @@ struct Signal {
   uint32_t status;                   // this rank's op status (0 = ok)
   uint32_t pad;
   pcclb_range range[kIpcMaxWorld + 1];  // range of the span sent at step s
+  pcclb_qmeta qmeta[kIpcMaxWorld];      // written by the predecessor: meta of its step-s codes
+  uint32_t claim[kIpcMaxWorld + 1];     // fused quantized steps + gather: work counters
+  pcclb_qmeta gmeta[kIpcMaxWorld];      // written by chunk c's owner: meta of its final codes
 };
 static_assert(sizeof(Signal) <= kSignalBytes, "signal area too small");
 
@@ -95,6 +103,13 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// polling: relaxed loads (no fence per poll), one acquire fence on success
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -589,6 +604,367 @@ __global__ void __launch_bounds__(kIpcThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused quantized reduce step (one kernel per ring step, no barrier).
+//
+// Step s of the reference's quantized ring (collective.py:521-536) on rank r:
+//   A: codes <- Q(buf[tx_s]) with the range the previous step produced, sent
+//      to the successor -- here pushed over NVLink into the successor's
+//      codes[s] with remote 16-byte stores, 64 Ki elements per block, each
+//      block followed by a ready token (st.release.sys) in its flags[s];
+//   B: buf[rx_s] <- buf[rx_s] (+) D(pred's codes[s]) for each block once the
+//      predecessor's token for it is visible (ld.acquire.sys), saving the old
+//      values (first touch of the rx chunk = the backup) and accumulating the
+//      range of the new partial for step s+1's quantization.
+// Work items are claimed in order from a per-step counter, A block j at
+// position 2j and B block j at 2j + 2*lag + 1, the same positions on every
+// rank. A items never wait, so a claimed B item always has its producer's A
+// item claimed or claimable on the predecessor (its position is smaller):
+// no cyclic wait, with any number of resident CTAs. The interleaving keeps
+// the NVLink pushes (A) and the HBM-bound accumulation (B) running at once.
+// Failures (fault injection, non-finite range, host abort, a peer's abort
+// token, timeout) set the status word and post abort tokens like the barrier
+// kernel; after a failure A items are skipped and B items only save the
+// backup, so the host restore finds every chunk's input.
+// ---------------------------------------------------------------------------
+struct QStepArgs {
+  const float *tx;            // this rank's tx chunk (caller buffer)
+  uint8_t *tcodes;            // successor's codes[s] at element 0 of the tx chunk
+  pcclb_qmeta *tmeta;         // successor's qmeta[s]
+  uint64_t *tflags;           // successor's flags[s]
+  const pcclb_range *trange;  // range of the tx chunk (previous step)
+  float *rx;                  // rx chunk (caller buffer)
+  float *rbak;                // backup of the rx chunk
+  const uint8_t *rcodes;      // own codes[s] at element 0 of the rx chunk
+  const pcclb_qmeta *rmeta;   // own qmeta[s]
+  const uint64_t *rflags;     // own flags[s]
+  pcclb_range *rrange;        // range of the new partial (next step)
+  Signal *mine;
+  Signal *peer[kIpcMaxWorld];
+  const HostFlags *host;
+  uint32_t *claim;
+  uint64_t tlo, tn, rlo, rn;
+  uint64_t token, attempt, timeout_ns;
+  uint32_t rank, world, fault, lag;
+  uint32_t tvec, rvec;  // 16-element vector bodies usable on the A / B side
+  uint32_t dbg;         // experiments (PCCLB_QDEBUG bits): 1 = B never waits, 2 = A stores locally
+};
+
+__device__ __forceinline__ uint64_t qblocks(uint64_t lo, uint64_t n) {
+  return n ? (lo + n - 1) / kQB - lo / kQB + 1 : 0;
+}
+// chunk-relative element range of block j (blocks follow the global kQB grid,
+// so producer and consumer agree whatever their buffers' alignment)
+__device__ __forceinline__ void qblock_range(uint64_t lo, uint64_t n, uint64_t j, uint64_t &i0, uint64_t &i1) {
+  const uint64_t k = lo / kQB + j;
+  uint64_t g0 = k * kQB, g1 = g0 + kQB;
+  if (g0 < lo) g0 = lo;
+  if (g1 > lo + n) g1 = lo + n;
+  i0 = g0 - lo;
+  i1 = g1 - lo;
+}
+
+template <class A>
+__device__ __forceinline__ void qfail(const A &a, uint32_t v) {
+  if (atomicCAS(&a.mine->status, 0u, v) == 0u)
+    for (uint32_t j = 0; j < a.world; ++j)
+      if (j != a.rank) st_release_sys(&a.peer[j]->abort_tok[a.rank], a.attempt);
+}
+
+// thread 0: wait for the predecessor's ready token (0) or a failure (status)
+template <class A>
+__device__ uint32_t qwait(const A &a, const uint64_t *flag) {
+  uint32_t rc = 0;
+  if (ld_relaxed_sys(flag) < a.token) {
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 64;
+    for (uint32_t it = 0;; ++it) {
+      __nanosleep(ns);
+      if (ns < 1024) ns *= 2;
+      if (ld_relaxed_sys(flag) >= a.token) break;
+      const uint32_t st = *(volatile uint32_t *)&a.mine->status;
+      if (st) return st;
+      if ((it & 7) == 0) {
+        if (a.host->abort) return PCCLB_EABORTED;
+        for (uint32_t j = 0; j < a.world; ++j)
+          if (j != a.rank && ld_relaxed_sys(&a.mine->abort_tok[j]) == a.attempt) return PCCLB_EABORTED;
+        if (globaltimer() - t0 > a.timeout_ns) return PCCLB_ETIMEOUT;
+      }
+    }
+  }
+  fence_acq_rel_sys();  // acquire: the block's codes and meta are visible after this
+  return rc;
+}
+
+// CTA-wide loop over chunk-relative elements [i0, i1): 16-element vectors
+// where the global index is a multiple of 16, scalar head and tail
+template <int U, typename F>
+__device__ __forceinline__ void cta_loop16(uint64_t lo, uint64_t i0, uint64_t i1, bool vec, F &f) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (!vec) {
+    for (uint64_t i = i0 + t; i < i1; i += nt) f.one(i);
+    return;
+  }
+  uint64_t head = (16 - ((lo + i0) & 15)) & 15;
+  if (head > i1 - i0) head = i1 - i0;
+  if (t < head) f.one(i0 + t);
+  const uint64_t b = i0 + head;
+  const uint64_t nv = (i1 - b) / 16;
+  uint64_t v = t;
+  for (; v + (U - 1) * nt < nv; v += U * nt) {
+    typename F::In in[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) in[u] = f.vload(b + (v + u * nt) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) f.vapply(b + (v + u * nt) * 16, in[u]);
+  }
+  for (; v < nv; v += nt) {
+    typename F::In in = f.vload(b + v * 16);
+    f.vapply(b + v * 16, in);
+  }
+  const uint64_t t0 = b + nv * 16;
+  if (t0 + t < i1) f.one(t0 + t);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kQThreads, 4) ipc_qstep_kernel(const __grid_constant__ QStepArgs a) {
+  __shared__ uint32_t s_item, s_ok;
+  const uint64_t nA = qblocks(a.tlo, a.tn), nB = qblocks(a.rlo, a.rn);
+  uint64_t npos = 2 * nA;
+  if (nB && 2 * (nB + a.lag) > npos) npos = 2 * (nB + a.lag);
+  if (threadIdx.x == 0 && *(volatile uint32_t *)&a.mine->status == 0) {
+    if (blockIdx.x == 0 && a.fault) qfail(a, PCCLB_EIO);  // reference fault_hook
+    else if (a.tn && a.trange->nonfinite) qfail(a, PCCLB_ENONFINITE);
+  }
+  const QParams qp = qparams_from_range(*a.trange);
+  RangeAcc racc;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const uint32_t it = atomicAdd(a.claim, 1u);
+      uint32_t ok = *(volatile uint32_t *)&a.mine->status == 0;
+      if ((it & 1) && it < npos) {
+        const uint64_t q = (it - 1) / 2;
+        if (q >= a.lag && q - a.lag < nB && ok && !(a.dbg & 1)) {
+          const uint32_t st = qwait(a, a.rflags + (q - a.lag));
+          if (st) {
+            qfail(a, st);
+            ok = 0;
+          }
+        }
+      }
+      s_item = it;
+      s_ok = ok;
+    }
+    __syncthreads();
+    const uint32_t it = s_item;
+    const bool ok = s_ok != 0;
+    __syncthreads();
+    if (it >= npos) break;
+    uint64_t i0, i1;
+    if (!(it & 1)) {
+      const uint64_t j = it / 2;
+      if (j >= nA || !ok) continue;
+      qblock_range(a.tlo, a.tn, j, i0, i1);
+      Quant16F f{a.tx, (a.dbg & 2) ? const_cast<uint8_t *>(a.rcodes) : a.tcodes, nullptr, qp, 1.0f, false};
+      cta_loop16<2>(a.tlo, i0, i1, a.tvec != 0, f);
+      __syncthreads();  // every thread's remote stores precede the token
+      if (threadIdx.x == 0) {
+        volatile pcclb_qmeta *m = a.tmeta;
+        m->min_val = qp.mn;
+        m->scale = qp.scale;
+        // release (cumulative over the CTA's stores, ordered by the barrier)
+        st_release_sys(a.tflags + j, a.token);
+      }
+    } else {
+      const uint64_t q = (it - 1) / 2;
+      if (q < a.lag || q - a.lag >= nB) continue;
+      const uint64_t j = q - a.lag;
+      qblock_range(a.rlo, a.rn, j, i0, i1);
+      if (!ok) {  // no accumulate, but the restore needs this block's input
+        CopyF f{a.rx, a.rbak};
+        for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) f.one(i);
+        continue;
+      }
+      const volatile pcclb_qmeta *m = a.rmeta;
+      // plain arithmetic: a NaN here makes the next range non-finite -> abort + restore
+      DequantAcc16F<OP, false> f{a.rx, a.rcodes, m->min_val, m->scale, racc, a.rbak};
+      cta_loop16<2>(a.rlo, i0, i1, a.rvec != 0, f);
+      racc = f.r;
+    }
+  }
+  range_block_commit(racc, a.rrange);
+}
+
+// ---------------------------------------------------------------------------
+// Fused gather (quantized): the owner's adoption and the W-1 dequantizing
+// copies in one kernel, without the barrier between them.
+//   A' (owner of chunk own = rank+1, collective.py:538-551): codes <- Q(own)
+//      with the last step's range, own <- D(codes) / W in place, and the codes
+//      pushed into every peer's gcodes[own] (remote 16-byte stores), one
+//      ready token per 64 Ki-element block in each peer's gflags[own];
+//   B' (collective.py:553-565): for every other chunk c, buf[c] <- D(gcodes[c])
+//      (/ W) once its owner's token for the block is visible.
+// Positions: round r holds W slots, slot 0 = A' block r, slot k >= 1 = block
+// r - lag of chunk (own + k) mod W; the owner's A' block j (position W*j)
+// precedes every B' item that waits for it (W*(j+lag)+k) on every rank, so
+// claims in position order cannot wait cyclically (see ipc_qstep_kernel).
+// ---------------------------------------------------------------------------
+struct QFinalArgs {
+  float *buf;
+  uint64_t lo[kIpcMaxWorld + 1];  // chunk bounds: chunk c = [lo[c], lo[c+1])
+  const pcclb_range *orange;      // range of the own chunk's final partial
+  uint64_t gcodes_off, codes_stride, gflags_off, flags_stride;  // workspace offsets (same on every rank)
+  Signal *mine;
+  Signal *peer[kIpcMaxWorld];     // peer workspaces (Signal at offset 0)
+  const HostFlags *host;
+  uint32_t *claim;
+  uint64_t token, attempt, timeout_ns;
+  uint32_t rank, world, own, fault, lag, vec;
+  float avg;  // 1: no division
+  uint32_t do_div;
+  uint32_t dbg;  // experiments (PCCLB_QDEBUG bit 0): B' never waits
+};
+
+__device__ __forceinline__ uint8_t *gcodes_of(const QFinalArgs &a, Signal *ws, uint32_t c) {
+  return reinterpret_cast<uint8_t *>(ws) + a.gcodes_off + c * a.codes_stride + a.lo[c] % 16;
+}
+__device__ __forceinline__ uint64_t *gflags_of(const QFinalArgs &a, Signal *ws, uint32_t c) {
+  return reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(ws) + a.gflags_off + c * a.flags_stride);
+}
+
+// quantize + adopt in place + push the codes to every peer
+template <bool X86>
+struct QuantPushF {
+  const QFinalArgs *a;
+  float *x;
+  QParams qp;
+  uint64_t coff;  // chunk's code offset inside a peer's workspace
+  __device__ __forceinline__ float adopt_val(uint32_t q) {
+    float d = dequant1x<X86>(q, qp.mn, qp.scale);
+    return a->do_div ? div_world_x<X86>(d, a->avg) : d;
+  }
+  __device__ __forceinline__ void one(uint64_t i) {
+    const uint32_t q = quant1_fast(x[i], qp.mn, qp.scale, qp.inv);
+    x[i] = adopt_val(q);
+    for (uint32_t p = 0; p < a->world; ++p)
+      if (p != a->rank) (reinterpret_cast<uint8_t *>(a->peer[p]) + coff)[i] = (uint8_t)q;
+  }
+  struct In {
+    Pack16<float> v[4];
+  };
+  __device__ __forceinline__ In vload(uint64_t i) {
+    In r;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) r.v[g] = ld16(x + i + 4 * g);
+    return r;
+  }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &in) {
+    uint32_t w[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint32_t q[4];
+      Pack16<float> d;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        q[k] = quant1_fast(in.v[g].e[k], qp.mn, qp.scale, qp.inv);
+        d.e[k] = adopt_val(q[k]);
+      }
+      w[g] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+      st16(x + i + 4 * g, d);
+    }
+    const uint4 c = make_uint4(w[0], w[1], w[2], w[3]);
+    for (uint32_t p = 0; p < a->world; ++p)
+      if (p != a->rank) *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a->peer[p]) + coff + i) = c;
+  }
+};
+
+__global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_constant__ QFinalArgs a) {
+  __shared__ uint32_t s_item, s_ok;
+  const uint32_t w = a.world, own = a.own;
+  const uint64_t olo = a.lo[own], on = a.lo[own + 1] - olo;
+  const uint64_t nO = qblocks(olo, on);
+  uint64_t rounds = nO, maxg = 0;
+  for (uint32_t k = 1; k < w; ++k) {
+    const uint32_t c = (own + k) % w;
+    const uint64_t nb = qblocks(a.lo[c], a.lo[c + 1] - a.lo[c]);
+    maxg = nb > maxg ? nb : maxg;
+  }
+  if (maxg && maxg + a.lag > rounds) rounds = maxg + a.lag;
+  const uint64_t npos = rounds * w;
+  if (threadIdx.x == 0 && *(volatile uint32_t *)&a.mine->status == 0) {
+    if (blockIdx.x == 0 && a.fault) qfail(a, PCCLB_EIO);
+    else if (a.host->abort) qfail(a, PCCLB_EABORTED);
+    else if (on && a.orange->nonfinite) qfail(a, PCCLB_ENONFINITE);
+  }
+  const QParams qp = qparams_from_range(*a.orange);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const uint32_t it = atomicAdd(a.claim, 1u);
+      uint32_t ok = *(volatile uint32_t *)&a.mine->status == 0;
+      const uint32_t k = it % w;
+      const uint64_t r = it / w;
+      if (k && it < npos && ok && r >= a.lag && !(a.dbg & 1)) {
+        const uint32_t c = (own + k) % w;
+        if (r - a.lag < qblocks(a.lo[c], a.lo[c + 1] - a.lo[c])) {
+          const uint32_t st = qwait(a, gflags_of(a, a.mine, c) + (r - a.lag));
+          if (st) {
+            qfail(a, st);
+            ok = 0;
+          }
+        }
+      }
+      s_item = it;
+      s_ok = ok;
+    }
+    __syncthreads();
+    const uint32_t it = s_item;
+    const bool ok = s_ok != 0;
+    __syncthreads();
+    if (it >= npos) break;
+    if (!ok) continue;  // every chunk's input is already in the backup
+    const uint32_t k = it % w;
+    const uint64_t r = it / w;
+    uint64_t i0, i1;
+    if (k == 0) {
+      if (r >= nO) continue;
+      qblock_range(olo, on, r, i0, i1);
+      const uint64_t coff = a.gcodes_off + own * a.codes_stride + olo % 16;
+      // finite scale and min: no NaN can arise (the x86 NaN rules only matter
+      // for an overflowed range, scale = inf)
+      if (finite_f(qp.scale) && finite_f(qp.mn)) {
+        QuantPushF<false> f{&a, a.buf + olo, qp, coff};
+        cta_loop16<2>(olo, i0, i1, a.vec != 0, f);
+      } else {
+        QuantPushF<true> f{&a, a.buf + olo, qp, coff};
+        cta_loop16<2>(olo, i0, i1, a.vec != 0, f);
+      }
+      __syncthreads();
+      if (threadIdx.x < w && threadIdx.x != a.rank) {
+        Signal *p = a.peer[threadIdx.x];
+        volatile pcclb_qmeta *m = &p->gmeta[own];
+        m->min_val = qp.mn;
+        m->scale = qp.scale;
+        st_release_sys(gflags_of(a, p, own) + r, a.token);
+      }
+    } else {
+      if (r < a.lag) continue;
+      const uint32_t c = (own + k) % w;
+      const uint64_t clo = a.lo[c], cn = a.lo[c + 1] - clo;
+      if (r - a.lag >= qblocks(clo, cn)) continue;
+      qblock_range(clo, cn, r - a.lag, i0, i1);
+      const volatile pcclb_qmeta *m = &a.mine->gmeta[c];
+      const float mn = m->min_val, sc = m->scale;
+      if (finite_f(sc) && finite_f(mn)) {
+        Dequant16T<false> f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
+        cta_loop16<2>(clo, i0, i1, a.vec != 0, f);
+      } else {
+        Dequant16F f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
+        cta_loop16<2>(clo, i0, i1, a.vec != 0, f);
+      }
+    }
+  }
+}
+
 }  // namespace pcclb
 
 using namespace pcclb;
@@ -644,6 +1020,7 @@ struct pcclb_ring {
   OpRec ops[kMaxOps];
   cudaEvent_t op_events[kMaxOps];
   uint32_t next_ticket = 0;
+  uint32_t slots = 2;  // engines that may run ops concurrently on this GPU (pcclb_ring_set_slots)
   uint64_t last_n;
   int last_dtype;
   bool have_backup;
@@ -654,7 +1031,9 @@ static Signal *sig_of(char *base) { return reinterpret_cast<Signal *>(base); }
 namespace {
 
 struct Layout {
-  uint64_t in, res, codes0, codes1, codesF, end;
+  uint64_t in, res, codes, codes_stride, codesF, flags, flags_stride, gcodes, gflags, end;
+  uint64_t codes_step(uint32_t s) const { return codes + s * codes_stride; }
+  uint64_t flags_step(uint32_t s) const { return flags + s * flags_stride; }
 };
 
 // Chunk-local buffers keep the chunk's sub-16-byte alignment (floats) or
@@ -673,12 +1052,20 @@ Layout layout_for(uint64_t n, uint32_t w, size_t esz, bool quant) {
     L.res = off;
     off = up(off + nc * esz + 16);
   } else {
-    L.codes0 = off;
-    off = up(off + nc + 16);
-    L.codes1 = off;
-    off = up(off + nc + 16);
+    const uint32_t steps = w > 1 ? w - 1 : 1;
+    L.codes = off;
+    L.codes_stride = up(nc + 16);
+    off += steps * L.codes_stride;
     L.codesF = off;
     off = up(off + nc + 16);
+    L.flags = off;
+    L.flags_stride = up((nc / kQB + 3) * 8);
+    off += steps * L.flags_stride;
+    // fused gather: every chunk's final codes, pushed by its owner
+    L.gcodes = off;
+    off += w * L.codes_stride;
+    L.gflags = off;
+    off += w * L.flags_stride;
   }
   L.end = off;
   return L;
@@ -939,6 +1326,17 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   return PCCLB_OK;
 }
 
+// fused quantized steps (default) or the barrier-per-step schedule
+// (PCCLB_QSTEP=0, and when too many engines may run at once for the fused
+// kernel's spinning CTAs to leave room for the others)
+bool qstep_enabled() {
+  static bool on = [] {
+    const char *e = getenv("PCCLB_QSTEP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t attempt, int fault_at,
                     uint64_t timeout_ns, cudaStream_t s) {
   const uint32_t w = r->world, rank = r->rank;
@@ -946,15 +1344,40 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   uint64_t lo[2 * kIpcMaxWorld];
   pcclb_chunk_bounds(n, w, lo);
   Signal *me = sig_of(r->ws);
-  const uint32_t pred = (rank + w - 1) % w;
+  const uint32_t pred = (rank + w - 1) % w, succ = (rank + 1) % w;
   Signal *pred_sig = sig_of(r->peer_ws[pred]);
   r->timer.mark(s);
   // no copy-in: every chunk's input is saved into `in` by the first kernel
   // that reads it (range for chunk `rank`, the step's dequant-accumulate for
   // each rx chunk), which also runs when the op already failed
   float *bak = reinterpret_cast<float *>(r->ws + L.in);
-  // range slots reset
+  // range slots and step counters reset; ready flags cleared (peers write
+  // them only after barrier 0, which this rank reaches after the memset)
   PCCLB_CUDA(cudaMemsetAsync(me->range, 0, sizeof(pcclb_range) * (w + 1), s));
+  static const int occ_q = [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ipc_qstep_kernel<PCCLB_SUM>, kQThreads, 0);
+    return o < 1 ? 1 : o;
+  }();
+  static const int slots_env = [] {
+    const char *e = getenv("PCCLB_QSLOTS");
+    return e ? atoi(e) : 0;
+  }();
+  // CTAs per SM for this engine's fused steps: the other slots' engines
+  // (spinning the same way) must still find a free CTA slot on every SM,
+  // (slots - 1) * per_sm <= occ - 1, so every engine's kernel makes progress
+  const int slots = slots_env > 0 ? slots_env : (int)(r->slots ? r->slots : 1);
+  const int per_sm = slots <= 1 ? occ_q : (occ_q - 1) / (slots - 1) < occ_q ? (occ_q - 1) / (slots - 1) : occ_q;
+  const bool fused = qstep_enabled() && per_sm >= 1;
+  static const uint32_t dbg = [] {
+    const char *e = getenv("PCCLB_QDEBUG");
+    return e ? (uint32_t)atoi(e) : 0u;
+  }();
+  if (fused) {
+    PCCLB_CUDA(cudaMemsetAsync(me->claim, 0, sizeof(uint32_t) * (w + 1), s));
+    PCCLB_CUDA(cudaMemsetAsync(r->ws + L.flags, 0, L.flags_stride * (w - 1), s));
+    PCCLB_CUDA(cudaMemsetAsync(r->ws + L.gflags, 0, L.flags_stride * w, s));
+  }
   auto span = [&](uint32_t c, uint64_t &a, uint64_t &len) {
     a = lo[2 * c];
     len = lo[2 * c + 1] - lo[2 * c];
@@ -967,13 +1390,69 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   }
   r->timer.mark(s);
   int rc;
+  if (fused) {
+    rc = launch_barrier(r, attempt, 0, fault_at, &me->range[0], timeout_ns, s,
+                        param_tag(n, PCCLB_F32, op, true), true);
+    if (rc) return rc;
+    r->timer.mark(s);
+    QStepArgs q{};
+    q.mine = me;
+    for (uint32_t j = 0; j < w; ++j) q.peer[j] = sig_of(r->peer_ws[j]);
+    q.host = r->host_dev;
+    q.token = attempt;
+    q.attempt = attempt;
+    q.timeout_ns = timeout_ns;
+    q.rank = rank;
+    q.world = w;
+    const unsigned grid = (unsigned)(sm_count() * per_sm);
+    static const double lag_mul = [] {
+      const char *e = getenv("PCCLB_QLAG");
+      return e ? atof(e) : 2.0;
+    }();
+    q.lag = (uint32_t)(grid * lag_mul);
+    q.dbg = dbg;
+    const bool buf_vec = (reinterpret_cast<uintptr_t>(buf) & 63) == 0;
+    for (uint32_t step = 0; step + 1 < w; ++step) {
+      const uint32_t tx = (rank + w - step % w) % w;     // (rank - step) mod w
+      const uint32_t rx = (rank + 2 * w - step - 1) % w;  // (rank - step - 1) mod w
+      span(tx, q.tlo, q.tn);
+      span(rx, q.rlo, q.rn);
+      q.tx = buf + q.tlo;
+      q.tcodes = reinterpret_cast<uint8_t *>(r->peer_ws[succ] + codes_at(L.codes_step(step), q.tlo));
+      q.tmeta = &sig_of(r->peer_ws[succ])->qmeta[step];
+      q.tflags = reinterpret_cast<uint64_t *>(r->peer_ws[succ] + L.flags_step(step));
+      q.trange = &me->range[step];
+      q.rx = buf + q.rlo;
+      q.rbak = bak + q.rlo;
+      q.rcodes = reinterpret_cast<const uint8_t *>(r->ws + codes_at(L.codes_step(step), q.rlo));
+      q.rmeta = &me->qmeta[step];
+      q.rflags = reinterpret_cast<const uint64_t *>(r->ws + L.flags_step(step));
+      q.rrange = &me->range[step + 1];
+      q.claim = &me->claim[step];
+      q.fault = (step > 0 && fault_at >= 0 && (uint32_t)fault_at == step) ? 1u : 0u;
+      q.tvec = q.rvec = buf_vec ? 1u : 0u;
+      switch (op) {
+        case PCCLB_MAX:
+          ipc_qstep_kernel<PCCLB_MAX><<<grid, kQThreads, 0, s>>>(q);
+          break;
+        case PCCLB_MIN:
+          ipc_qstep_kernel<PCCLB_MIN><<<grid, kQThreads, 0, s>>>(q);
+          break;
+        default:
+          ipc_qstep_kernel<PCCLB_SUM><<<grid, kQThreads, 0, s>>>(q);
+          break;
+      }
+      PCCLB_LAUNCH_CHECK();
+      r->timer.mark(s);
+    }
+  } else {
   for (uint32_t step = 0; step + 1 < w; ++step) {
     const uint32_t tx = (rank + w - step % w) % w;         // (rank - step) mod w
     const uint32_t rx = (rank + 2 * w - step - 1) % w;      // (rank - step - 1) mod w
     uint64_t ta, tn, ra, rn;
     span(tx, ta, tn);
     span(rx, ra, rn);
-    const uint64_t codes_off = (step & 1) ? L.codes1 : L.codes0;
+    const uint64_t codes_off = L.codes_step(step);
     // quantize what we send (its range was produced by the previous step)
     ipc_quantize_kernel<<<ipc_grid(tn / 4 + 1), kIpcThreads, 0, s>>>(
         buf + ta, tn, &me->range[step], reinterpret_cast<uint8_t *>(r->ws + codes_at(codes_off, ta)),
@@ -1002,9 +1481,46 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
       PCCLB_LAUNCH_CHECK();
     }
   }
+  }
   r->timer.mark(s);
-  // gather prologue: owner adopts D(Q(own)) (collective.py:538-551), fused with AVG
   const uint32_t own = (rank + 1) % w;
+  if (fused) {
+    QFinalArgs g{};
+    g.buf = buf;
+    for (uint32_t c = 0; c < w; ++c) g.lo[c] = lo[2 * c];
+    g.lo[w] = n;
+    g.orange = &me->range[w - 1];
+    g.gcodes_off = L.gcodes;
+    g.codes_stride = L.codes_stride;
+    g.gflags_off = L.gflags;
+    g.flags_stride = L.flags_stride;
+    g.mine = me;
+    for (uint32_t j = 0; j < w; ++j) g.peer[j] = sig_of(r->peer_ws[j]);
+    g.host = r->host_dev;
+    g.claim = &me->claim[w - 1];
+    g.token = attempt;
+    g.attempt = attempt;
+    g.timeout_ns = timeout_ns;
+    g.rank = rank;
+    g.world = w;
+    g.own = own;
+    g.fault = (fault_at >= 0 && (uint32_t)fault_at == w - 1) ? 1u : 0u;
+    const unsigned grid = (unsigned)(sm_count() * per_sm);
+    static const double glag = [] {
+      const char *e = getenv("PCCLB_GLAG");
+      return e ? atof(e) : 8.0;  // measured: 2 -> 2.26 ms, 8 -> 1.98 ms (W=2, 1.2 B elements)
+    }();
+    g.lag = (uint32_t)((glag * grid + w - 1) / w);  // rounds of w positions
+    g.dbg = dbg;
+    g.vec = (reinterpret_cast<uintptr_t>(buf) & 63) == 0 ? 1u : 0u;
+    g.avg = (op == PCCLB_AVG) ? (float)w : 1.0f;
+    g.do_div = op == PCCLB_AVG ? 1u : 0u;
+    ipc_qfinal_kernel<<<grid, kQThreads, 0, s>>>(g);
+    PCCLB_LAUNCH_CHECK();
+    r->timer.mark(s);
+    return PCCLB_OK;
+  }
+  // gather prologue: owner adopts D(Q(own)) (collective.py:538-551), fused with AVG
   uint64_t oa, on;
   span(own, oa, on);
   const uint32_t avg = (op == PCCLB_AVG) ? w : 1;
@@ -1117,6 +1633,12 @@ int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle64) {
   PCCLB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   r->peer_ws[peer] = static_cast<char *>(p);
   r->imported[peer] = true;
+  return PCCLB_OK;
+}
+
+int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots) {
+  if (!r || slots < 1) return PCCLB_EINVAL;
+  r->slots = slots;
   return PCCLB_OK;
 }
 

@@ -64,7 +64,7 @@ class DeviceRing:
     """
 
     def __init__(self, group=None, ring: list[int] | None = None, device=None,
-                 capacity_bytes: int = 64 << 20, timeout_s: float = 60.0):
+                 capacity_bytes: int = 64 << 20, timeout_s: float = 60.0, slots: int = 2):
         if not dist.is_initialized():
             raise UsageError("torch.distributed must be initialized")
         self.group = group
@@ -81,6 +81,8 @@ class DeviceRing:
         self._handle = None
         self._capacity = 0
         self._registered: dict[int, torch.Tensor] = {}  # slot -> tensor (kept alive)
+        # engines sharing this GPU concurrently (the communicator's pool size)
+        self.slots = max(1, int(slots))
         self._create(capacity_bytes)
 
     # -- workspace lifecycle (collective: every rank calls in the same order) --
@@ -93,6 +95,7 @@ class DeviceRing:
         )
         self._handle = h
         self._capacity = capacity_bytes
+        check(lib().pcclb_ring_set_slots(h, self.slots), "ring_set_slots")
         mine = ctypes.create_string_buffer(64)
         check(lib().pcclb_ring_export(h, mine), "ring_export")
         handles = exchange_bytes(bytes(mine.raw), self.group)  # indexed by group rank
@@ -119,13 +122,21 @@ class DeviceRing:
         except Exception:
             pass
 
+    @staticmethod
+    def required_bytes(n: int, world: int, esz: int, quantize: bool) -> int:
+        """Workspace bytes for an n-element op (upper bound of the engine's layout)."""
+        nc = (n + world - 1) // world
+        need = 16384 + n * esz + 4 * nc * esz + 4096
+        if quantize:  # step codes, final codes, gathered codes + ready flags
+            need += 2 * world * (nc + 512) + 2 * world * (nc // 65536 + 3) * 8
+        return int(need * 1.02)
+
     def ensure_capacity(self, n: int, dtype: torch.dtype, quantize: bool) -> None:
         code = DTYPE_CODE[dtype]
         if lib().pcclb_ring_capacity(self._handle, code, int(quantize)) >= n:
             return
         esz = torch.tensor([], dtype=dtype).element_size()
-        need = 16384 + n * esz + 4 * ((n + self.world - 1) // self.world) * max(esz, 1) + 4096
-        self._create(int(need * 1.05))
+        self._create(self.required_bytes(n, self.world, esz, quantize))
 
     # -- caller-buffer registration (collective, SPMD order) --
     def register(self, tensor: torch.Tensor) -> int:

@@ -15,7 +15,7 @@ rank, world, local = init_from_env("gloo")
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 28
 dev = torch.device("cuda", local)
 buf = torch.randn(n, device=dev)
-ring = DeviceRing(device=dev, capacity_bytes=16384 + n * 4 + 4 * (n // world + 1) * 4 + (1 << 20))
+ring = DeviceRing(device=dev, capacity_bytes=DeviceRing.required_bytes(n, world, 4, False))
 if os.environ.get("REGISTER", "1") == "1":
     ring.register(buf)
 for _ in range(3):

@@ -18,7 +18,7 @@ quant = len(sys.argv) > 2 and sys.argv[2] == "quant"
 op = sys.argv[3] if len(sys.argv) > 3 else "avg"
 dev = torch.device("cuda", local)
 buf = torch.randn(n, device=dev) * (1e-2 if quant else 1)
-ring = DeviceRing(device=dev, capacity_bytes=16384 + n * 4 + 4 * (n // world + 1) * 4 + (1 << 20))
+ring = DeviceRing(device=dev, capacity_bytes=DeviceRing.required_bytes(n, world, 4, quant))
 if os.environ.get("REGISTER", "1") == "1":
     ring.register(buf)
 rows = []
