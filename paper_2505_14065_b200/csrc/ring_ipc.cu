@@ -109,7 +109,6 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p) {
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -692,7 +691,9 @@ __device__ uint32_t qwait(const A &a, const uint64_t *flag) {
       }
     }
   }
-  fence_acq_rel_sys();  // acquire: the block's codes and meta are visible after this
+  // acquire (an acquire load, not a fence: no MEMBAR behind this CTA's own
+  // outstanding stores): the block's codes and meta are visible after this
+  (void)ld_acquire_sys(flag);
   return rc;
 }
 
