@@ -364,7 +364,9 @@ def bench_allreduce(args, rank, world, local, quantize=False):
         e2e = {"value": round(e2e_alg * 2 * (world - 1) / world if world > 1 else e2e_alg, 2), "unit": "GB/s",
                "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3)}
     nvl_bytes = 2 * (world - 1) / world * S  # per-GPU NVLink ingress (plain)
-    launches_per_op = (2 + 2 + 1) if not quantize else (1 + 3 * (world - 1) + 2 + 1)
+    # plain: fold, push gather, 3 barriers; quantized (fused schedule): range,
+    # barrier 0, W-1 step kernels, the fused adoption+gather kernel
+    launches_per_op = (2 + 3) if not quantize else (1 + 1 + (world - 1) + 1)
     if not quantize:
         # NVLink-bound: per-GPU ingress 2(W-1)/W * S against the measured peer copy
         roof = {"bound": "nvlink", "achieved": round(nvl_bytes / (ms_max * 1e-3) / 1e9, 1),
@@ -385,6 +387,12 @@ def bench_allreduce(args, rank, world, local, quantize=False):
                 "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
                 "algorithmic_bytes_per_gpu": hbm_bytes,
                 "nvlink_bytes_per_gpu": 2 * (world - 1) * n_c}
+        # the schedule's own HBM traffic, incl. the backup the reference keeps
+        # (collective.py:501-504) and the codes peers push into this GPU:
+        # range+backup 8, per step 18, adoption 8, gather (W-1) x 6 B per n_c
+        full = (16 + 24 * (world - 1)) * n_c
+        roof["schedule_bytes_per_gpu"] = full
+        roof["frac_of_schedule_floor"] = round(full / (ms_max * 1e-3) / 1e9 / pk["hbm_gbs"], 4)
     result = {
         "value": round(busbw, 2),
         "unit": "GB/s",

@@ -71,8 +71,13 @@ namespace pcclb {
 
 constexpr int kIpcMaxWorld = 64;
 constexpr uint64_t kSignalBytes = 16384;
+#ifndef PCCLB_QB
+#define PCCLB_QB 65536
+#endif
 constexpr int kIpcThreads = 512;
-constexpr uint64_t kQB = 65536;  // elements per ready-flag block of the fused quantized steps
+constexpr uint64_t kQB = PCCLB_QB;  // elements per ready-flag block of the fused quantized steps
+// fused gather blocks: larger (fewer release fences; measured W=2: 64 Ki 1.92 ms, 256 Ki 1.80 ms)
+constexpr uint64_t kQF = 4 * kQB;
 constexpr int kQThreads = 256;
 
 struct Signal {
@@ -649,14 +654,15 @@ struct QStepArgs {
   uint32_t dbg;         // experiments (PCCLB_QDEBUG bits): 1 = B never waits, 2 = A stores locally
 };
 
-__device__ __forceinline__ uint64_t qblocks(uint64_t lo, uint64_t n) {
-  return n ? (lo + n - 1) / kQB - lo / kQB + 1 : 0;
+__device__ __forceinline__ uint64_t qblocks(uint64_t lo, uint64_t n, uint64_t qb = kQB) {
+  return n ? (lo + n - 1) / qb - lo / qb + 1 : 0;
 }
 // chunk-relative element range of block j (blocks follow the global kQB grid,
 // so producer and consumer agree whatever their buffers' alignment)
-__device__ __forceinline__ void qblock_range(uint64_t lo, uint64_t n, uint64_t j, uint64_t &i0, uint64_t &i1) {
-  const uint64_t k = lo / kQB + j;
-  uint64_t g0 = k * kQB, g1 = g0 + kQB;
+__device__ __forceinline__ void qblock_range(uint64_t lo, uint64_t n, uint64_t j, uint64_t &i0, uint64_t &i1,
+                                             uint64_t qb = kQB) {
+  const uint64_t k = lo / qb + j;
+  uint64_t g0 = k * qb, g1 = g0 + qb;
   if (g0 < lo) g0 = lo;
   if (g1 > lo + n) g1 = lo + n;
   i0 = g0 - lo;
@@ -883,11 +889,11 @@ __global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_c
   __shared__ uint32_t s_item, s_ok;
   const uint32_t w = a.world, own = a.own;
   const uint64_t olo = a.lo[own], on = a.lo[own + 1] - olo;
-  const uint64_t nO = qblocks(olo, on);
+  const uint64_t nO = qblocks(olo, on, kQF);
   uint64_t rounds = nO, maxg = 0;
   for (uint32_t k = 1; k < w; ++k) {
     const uint32_t c = (own + k) % w;
-    const uint64_t nb = qblocks(a.lo[c], a.lo[c + 1] - a.lo[c]);
+    const uint64_t nb = qblocks(a.lo[c], a.lo[c + 1] - a.lo[c], kQF);
     maxg = nb > maxg ? nb : maxg;
   }
   if (maxg && maxg + a.lag > rounds) rounds = maxg + a.lag;
@@ -906,7 +912,7 @@ __global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_c
       const uint64_t r = it / w;
       if (k && it < npos && ok && r >= a.lag && !(a.dbg & 1)) {
         const uint32_t c = (own + k) % w;
-        if (r - a.lag < qblocks(a.lo[c], a.lo[c + 1] - a.lo[c])) {
+        if (r - a.lag < qblocks(a.lo[c], a.lo[c + 1] - a.lo[c], kQF)) {
           const uint32_t st = qwait(a, gflags_of(a, a.mine, c) + (r - a.lag));
           if (st) {
             qfail(a, st);
@@ -928,7 +934,7 @@ __global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_c
     uint64_t i0, i1;
     if (k == 0) {
       if (r >= nO) continue;
-      qblock_range(olo, on, r, i0, i1);
+      qblock_range(olo, on, r, i0, i1, kQF);
       const uint64_t coff = a.gcodes_off + own * a.codes_stride + olo % 16;
       // finite scale and min: no NaN can arise (the x86 NaN rules only matter
       // for an overflowed range, scale = inf)
@@ -951,8 +957,8 @@ __global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_c
       if (r < a.lag) continue;
       const uint32_t c = (own + k) % w;
       const uint64_t clo = a.lo[c], cn = a.lo[c + 1] - clo;
-      if (r - a.lag >= qblocks(clo, cn)) continue;
-      qblock_range(clo, cn, r - a.lag, i0, i1);
+      if (r - a.lag >= qblocks(clo, cn, kQF)) continue;
+      qblock_range(clo, cn, r - a.lag, i0, i1, kQF);
       const volatile pcclb_qmeta *m = &a.mine->gmeta[c];
       const float mn = m->min_val, sc = m->scale;
       if (finite_f(sc) && finite_f(mn)) {
@@ -1509,7 +1515,7 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     const unsigned grid = (unsigned)(sm_count() * per_sm);
     static const double glag = [] {
       const char *e = getenv("PCCLB_GLAG");
-      return e ? atof(e) : 8.0;  // measured: 2 -> 2.26 ms, 8 -> 1.98 ms (W=2, 1.2 B elements)
+      return e ? atof(e) : 4.0;  // measured (64 Ki blocks): 2 -> 2.26 ms, 8 -> 1.98 ms (W=2, 1.2 B elements)
     }();
     g.lag = (uint32_t)((glag * grid + w - 1) / w);  // rounds of w positions
     g.dbg = dbg;

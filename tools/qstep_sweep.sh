@@ -7,7 +7,7 @@ port=29600
 run() {
   port=$((port+1))
   echo "== $*"
-  env "$@" timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+  env "$@" timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node ${N} --master-addr 127.0.0.1 \
     --master-port $port tools/ring_phases.py $ELEMS quant 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['total_ms'], d['phase_ms_per_rank'][0])"
 }
 run PCCLB_QSTEP=0
