@@ -177,6 +177,26 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             check("registration mismatch rejected", rejected)
             check("registration mismatch intact", target.cpu().numpy().tobytes() == inputs[ring.position].tobytes())
             ring.deregister(0)
+        if "qedge" in scenarios:
+            # quantized schedule variants: fused at 3 and 4 CTAs/SM (slots 2, 1) and the
+            # barrier-per-step fallback (slots 5); misaligned views, chunks shorter than
+            # a ready-flag block, sizes straddling block boundaries, every op
+            cases = [(1, 0, "sum"), (world - 1, 1, "avg"), (7, 1, "max"), (65536 * world + 5, 1, "min"),
+                     (3 * 65536 * world + 17, 3, "avg"), ((1 << 20) + 3, 0, "sum"),
+                     (2 * 262144 * world + 9, 2, "avg"), (262144 * world - 1, 0, "max")]
+            for slots in (2, 1, 5):
+                eng = DeviceRing(device=dev, capacity_bytes=64 << 20, timeout_s=20.0, slots=slots)
+                for ci, (n, off, op) in enumerate(cases):
+                    inputs = ring_inputs(world, n, np.dtype("float32"), 700 + ci)
+                    base = torch.zeros(n + 8, device=dev)
+                    view = base[off:off + n]
+                    view.copy_(torch.from_numpy(inputs[eng.position]))
+                    eng.run_all_reduce(view, op, quantize=True)
+                    want = oring.ring_allreduce_chunkwise(inputs, getattr(oring.ReduceOp, op.upper()), quantize=True)
+                    check(f"qedge slots={slots} n={n} off={off} {op}", view.cpu().numpy().tobytes() == want.tobytes())
+                    check(f"qedge slots={slots} n={n}: guard bytes", float(base[:off].abs().sum()) == 0.0
+                          and float(base[off + n:].abs().sum()) == 0.0)
+                eng.close()
         if "large" in scenarios:
             n = (1 << 24) + 3
             for quant in (False, True):
@@ -215,5 +235,5 @@ if __name__ == "__main__":
     import torch.multiprocessing as mp
 
     world, port, outdir = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-    scenarios = sys.argv[4:] or ["golden", "faults", "registered", "large"]
+    scenarios = sys.argv[4:] or ["golden", "faults", "registered", "qedge", "large"]
     mp.spawn(_entry, args=(world, port, outdir, scenarios), nprocs=world, join=True)
