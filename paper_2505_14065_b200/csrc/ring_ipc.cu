@@ -829,7 +829,8 @@ struct QFinalArgs {
   uint32_t rank, world, own, fault, lag, vec;
   float avg;  // 1: no division
   uint32_t do_div;
-  uint32_t dbg;  // experiments (PCCLB_QDEBUG bit 0): B' never waits
+  uint32_t dbg;  // experiments (PCCLB_QDEBUG bits): 1 B' never waits, 4 A' pushes to its own
+                 // workspace, 8 B' items skipped
 };
 
 __device__ __forceinline__ uint8_t *gcodes_of(const QFinalArgs &a, Signal *ws, uint32_t c) {
@@ -881,7 +882,8 @@ struct QuantPushF {
     }
     const uint4 c = make_uint4(w[0], w[1], w[2], w[3]);
     for (uint32_t p = 0; p < a->world; ++p)
-      if (p != a->rank) *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a->peer[p]) + coff + i) = c;
+      if (p != a->rank)
+        *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>((a->dbg & 4) ? a->mine : a->peer[p]) + coff + i) = c;
   }
 };
 
@@ -954,7 +956,7 @@ __global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_c
         st_release_sys(gflags_of(a, p, own) + r, a.token);
       }
     } else {
-      if (r < a.lag) continue;
+      if (r < a.lag || (a.dbg & 8)) continue;
       const uint32_t c = (own + k) % w;
       const uint64_t clo = a.lo[c], cn = a.lo[c + 1] - clo;
       if (r - a.lag >= qblocks(clo, cn, kQF)) continue;
