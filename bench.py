@@ -451,6 +451,68 @@ def bench_local(args, rank, world, local):
     }
 
 
+def bench_async(args, rank, world, local):
+    """Config 5 shape without the fault: two u8-quantized AVG all-reduces (tags 0
+    and 1, two halves of a pseudo-gradient) in flight together through the
+    Communicator API (client.py:802-847: one engine + stream per pool slot).
+    A step enqueues both and awaits both on the host."""
+    import torch
+
+    from paper_2505_14065_b200.communicator import Communicator
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n = args.elems or 600_000_000
+    g = torch.Generator(device=dev).manual_seed(rank)
+    src = [torch.randn(n, generator=g, device=dev) * 1e-2 for _ in range(2)]
+    bufs = [s.clone() for s in src]
+    comm = Communicator(device=dev, pool_size=2, capacity_bytes=DeviceRing.required_bytes(n, world, 4, True))
+
+    def step():
+        hs = [comm.all_reduce_async(bufs[t], t, "avg", quantize=True) for t in range(2)]
+        for h in hs:
+            r = comm.await_async_reduce(h)
+            if not r.completed:
+                raise RuntimeError(f"async all-reduce aborted: {r.reason}")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    for st in comm.streams:
+        stream.wait_stream(st)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    S = 2 * n * 4
+    algbw = S / (ms * 1e-3) / 1e9
+    busbw = algbw * 2 * (world - 1) / world if world > 1 else 0.0
+    n_c = (n + world - 1) // world
+    full = 2 * (16 + 24 * (world - 1)) * n_c  # the fused schedule's HBM traffic, both tags
+    pk = peaks()
+    comm.close()
+    return {
+        "value": round(busbw, 2), "unit": "GB/s", "ms_per_step": round(ms, 4), "scaling": "weak", "dtype": "f32",
+        "config": {"workload": f"config5 (no fault): two concurrent u8-quantized AVG all-reduces of {n} fp32 each "
+                               f"per GPU (tags 0/1, Communicator pool of 2), W={world}",
+                   "elements_per_gpu_per_tag": n, "algbw_GBps": round(algbw, 2), "busbw_definition": "algbw*2(W-1)/W",
+                   "timing": "host enqueue + await of both tags inside the timed region"},
+        "roofline": {"bound": "hbm", "achieved": round(full / (ms * 1e-3) / 1e9, 1), "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(full / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4), "traffic": None,
+                     "peak_src": pk["src"], "schedule_bytes_per_gpu": full},
+        "clocks": clk, "e2e": None, "gpu_launches": 2 * (world + 2) * args.steps,
+    }
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the reference algorithm on host cores (oracle port)
 # ---------------------------------------------------------------------------
@@ -485,7 +547,7 @@ def reference_arm(args, workload, world):
     n = 1 << 22  # bounded sample: 16 MiB per rank
     rng = np.random.default_rng(0)
     bufs = [rng.normal(0, 1, n).astype(np.float32) for _ in range(w)]
-    quant = workload == "quant"
+    quant = workload in ("quant", "async")
     oring.ring_allreduce(bufs, oring.ReduceOp.AVG, quantize=quant)
     steps = max(1, min(args.steps, 3))
     t = time.perf_counter()
@@ -508,7 +570,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "local"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "async", "local"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--elems", type=int, default=0, help="override elements per GPU (allreduce/quant/local)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -535,6 +597,8 @@ def main():
         res = bench_allreduce(args, rank, world, local, quantize=False)
     elif workload == "quant":
         res = bench_allreduce(args, rank, world, local, quantize=True)
+    elif workload == "async":
+        res = bench_async(args, rank, world, local)
     else:
         res = bench_local(args, rank, world, local)
     line = {"metric": METRIC, "value": res.pop("value"), "unit": res.pop("unit"), "n_gpus": world,
