@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o p2p_micro p2p_micro.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
@@ -20,6 +21,33 @@ __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ d
     for (int u = 0; u < U; ++u) dst[v + u * nth] = x[u];
   }
   for (; v < nv; v += nth) dst[v] = src[v];
+}
+
+// TMA bulk push: tiles staged in shared memory, one cp.async.bulk global<-shared
+// per tile to the destination (peer memory), NBUF tiles in flight per CTA
+template <int TILE, int NBUF>
+__global__ void tma_push_kernel(const uint4 *__restrict__ src, char *dst, uint64_t bytes) {
+  extern __shared__ __align__(128) char sm[];
+  const uint64_t ntiles = bytes / TILE;
+  int k = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    char *buf = sm + (k % NBUF) * TILE;
+    if (k >= NBUF) {
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NBUF - 1) : "memory");
+      __syncthreads();
+    }
+    const uint4 *s = src + t * (TILE / 16);
+    for (int i = threadIdx.x; i < TILE / 16; i += blockDim.x) reinterpret_cast<uint4 *>(buf)[i] = s[i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + t * TILE),
+                   "r"((uint32_t)__cvta_generic_to_shared(buf)), "r"(TILE)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int main() {
@@ -47,8 +75,10 @@ int main() {
         cudaSetDevice(d);
         cudaEventRecord(e0[d], st[d]);
         const uint4 *src = (const uint4 *)(mode == 0 || mode == 2 ? a[1 - d] : a[d]);
-        uint4 *dst = (uint4 *)(mode == 1 ? b[1 - d] : b[d]);
+        uint4 *dst = (uint4 *)(mode == 1 || mode == 3 ? b[1 - d] : b[d]);
         if (mode == 2) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st[d]);
+        else if (mode == 3 && unroll == 16) tma_push_kernel<16384, 4><<<grid, 256, 4 * 16384, st[d]>>>(src, (char *)dst, bytes);
+        else if (mode == 3) tma_push_kernel<32768, 4><<<grid, 256, 4 * 32768, st[d]>>>(src, (char *)dst, bytes);
         else if (unroll == 1) copy_kernel<1><<<grid, 512, 0, st[d]>>>(src, dst, nv);
         else if (unroll == 4) copy_kernel<4><<<grid, 512, 0, st[d]>>>(src, dst, nv);
         else copy_kernel<8><<<grid, 512, 0, st[d]>>>(src, dst, nv);
@@ -65,7 +95,18 @@ int main() {
     }
     return bytes / (best * 1e-3) / 1e9;
   };
+  for (int d = 0; d < 2; ++d) {
+    cudaSetDevice(d);
+    cudaFuncSetAttribute(tma_push_kernel<16384, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384);
+    cudaFuncSetAttribute(tma_push_kernel<32768, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32768);
+  }
+  for (int bidir = 0; bidir < 2; ++bidir)
+    for (int grid : {148, 296})
+      for (int tile : {16, 32})
+        printf("tma-push %s grid=%4d tile=%dKiB x4 : %7.1f GB/s per direction\n", bidir ? "bidir" : "unidir", grid, tile,
+               run(3, bidir, grid, tile));
   const char *names[3] = {"pull", "push", "CE"};
+  if (getenv("P2P_ONLY_TMA")) return 0;
   for (int mode = 0; mode < 3; ++mode)
     for (int bidir = 0; bidir < 2; ++bidir) {
       if (mode == 2) {
