@@ -120,6 +120,17 @@ class ClockSampler:
                 "source": "NVML (nvidia_ml_py), sampled during the timed region"}
 
 
+def ncu_traffic(key: str):
+    """DRAM bytes per launch of the workload's dominant kernel from the committed
+    ncu capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f).get(key)
+        return int(e["bytes"]) if e else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -257,7 +268,9 @@ def bench_hash(args, rank, world, local):
                    "entries": len(views), "bytes_per_gpu": nbytes, "largest_entry_bytes": views[0].numel() * 2,
                    "l2": "inputs 16 GB >> 126 MB L2; no flush needed", "replicas": world},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
+                     "frac": round(achieved / pk["hbm_gbs"], 4),
+                     "traffic": ncu_traffic("hash_config4"),
+                     "peak_src": pk["src"],
                      "kernel": "simplehash_batch_kernel", "algorithmic_bytes_per_launch": nbytes,
                      "largest_entry_alone_ms": round(big_ms, 3),
                      "largest_entry_alone_gbs": round(views[0].numel() * 2 / (big_ms * 1e-3) / 1e9, 1),
@@ -385,6 +398,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
         ach = hbm_bytes / (ms_max * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_src": pk["src"],
+                "traffic_step_kernel": (ncu_traffic("quant_w2_1200M_step") if world == 2 and n == 1_200_000_000 else None),
                 "algorithmic_bytes_per_gpu": hbm_bytes,
                 "nvlink_bytes_per_gpu": 2 * (world - 1) * n_c}
         # the schedule's own HBM traffic, incl. the backup the reference keeps
@@ -446,7 +460,9 @@ def bench_local(args, rank, world, local):
         "value": round(busbw, 2), "unit": "GB/s", "ms_per_step": round(ms, 4), "scaling": "weak", "dtype": "f32",
         "config": {"workload": "8 logical ring peers x 1 GiB fp32 on one GPU, AVG (RingSession shape)", "elements_per_peer": n},
         "roofline": {"bound": "hbm", "achieved": round(hbm, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(hbm / pk["hbm_gbs"], 4), "traffic": None, "kernel": "local_fold_all_kernel"},
+                     "frac": round(hbm / pk["hbm_gbs"], 4),
+                     "traffic": ncu_traffic("local_w8_1GiB") if n == 1 << 28 and w == 8 else None,
+                     "kernel": "local_fold_all_kernel"},
         "clocks": clk, "e2e": None, "gpu_launches": args.steps,
     }
 
