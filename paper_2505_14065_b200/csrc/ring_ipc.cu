@@ -1400,8 +1400,10 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
   r->timer.mark(s);
   int rc;
   if (fused) {
+    // descriptor bit 39: this rank runs the fused schedule (a rank on the
+    // barrier-per-step schedule publishes it clear -> EINVAL on both sides)
     rc = launch_barrier(r, attempt, 0, fault_at, &me->range[0], timeout_ns, s,
-                        param_tag(n, PCCLB_F32, op, true), true);
+                        param_tag(n, PCCLB_F32, op, true) | (1ull << 39), true);
     if (rc) return rc;
     r->timer.mark(s);
     QStepArgs q{};
