@@ -197,6 +197,19 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                     check(f"qedge slots={slots} n={n}: guard bytes", float(base[:off].abs().sum()) == 0.0
                           and float(base[off + n:].abs().sum()) == 0.0)
                 eng.close()
+            # ranks on different quantized schedules (rank 0 on the barrier fallback)
+            # must reject the op together and keep their bytes
+            eng = DeviceRing(device=dev, capacity_bytes=64 << 20, timeout_s=20.0, slots=5 if rank == 0 else 2)
+            inputs = ring_inputs(world, 10_001, np.dtype("float32"), 790)
+            buf = torch.from_numpy(inputs[eng.position].copy()).to(dev)
+            rejected = False
+            try:
+                eng.run_all_reduce(buf, "avg", quantize=True)
+            except (UsageError, CollectiveAborted):
+                rejected = True
+            check("qedge: schedule mismatch rejected", rejected)
+            check("qedge: schedule mismatch intact", buf.cpu().numpy().tobytes() == inputs[eng.position].tobytes())
+            eng.close()
         if "large" in scenarios:
             n = (1 << 24) + 3
             for quant in (False, True):
