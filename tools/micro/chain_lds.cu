@@ -173,7 +173,7 @@ __global__ void chain(int stages, uint64_t *out, long long *cyc) {
   long long t0 = clock64();
   for (int s = 0; s < stages; ++s) {
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) f.step(wds[r * 128]);
+    for (int r = 0; r < ROWS; ++r) f.step(wds[r * blockDim.x]);
     __syncwarp();
   }
   long long t1 = clock64();
@@ -192,6 +192,18 @@ int main() {
     long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("%-8s threads=%3d : %6.2f cycles/step\n", name, threads, (double)h / (stages * ROWS));
   };
+  auto runr = [&](auto kern, const char *name, int threads, int rows) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<1, threads, rows * threads * 4>>>(stages / 4, out, cyc);
+    cudaDeviceSynchronize();
+    long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-8s threads=%3d rows=%3d : %6.2f cycles/step\n", name, threads, rows, (double)h / (stages / 4 * rows));
+  };
+  // phase-1 shape: 64 lanes, 256 rows unrolled per stage
+  runr(chain<LoOnly, 256>, "lo-only", 64, 256);
+  runr(chain<LoOnly, 128>, "lo-only", 64, 128);
+  runr(chain<LoOnly, 64>, "lo-only", 64, 64);
+  runr(chain<LoOnly, 256>, "lo-only", 96, 256);
   for (int t : {128}) {
     run(chain<Cur, 64>, "cur", t);
     run(chain<LoOnly, 64>, "lo-only", t);
