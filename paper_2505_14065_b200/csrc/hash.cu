@@ -66,11 +66,14 @@ constexpr int kMaxBatch = 560;       // HashBatch must fit the 32 KiB kernel-par
 // phase-1 items: 64 lanes per CTA and 256-row boxes, so each lo chain CTA keeps
 // ~2.7 us of TMA in flight (the lo chain consumes 512 B per ~10.5 cycles per
 // 128 lanes, more than one CTA's stream of 128-lane boxes sustains)
-constexpr int kP1Lanes = 64;
-constexpr int kP1Rows = 256;
+#ifndef PCCLB_P1_LANES
+#define PCCLB_P1_LANES 32  // measured (one 1.05 GB entry): 64 lanes x 256 rows 6.06 ms, 32 x 512 5.74 ms
+#endif
+constexpr int kP1Lanes = PCCLB_P1_LANES;
+constexpr int kP1Rows = 256 * 64 / kP1Lanes;  // one 64 KiB stage
 constexpr int kP1Groups = 256 / kP1Lanes;
 #ifndef PCCLB_P1_UNROLL
-#define PCCLB_P1_UNROLL 256
+#define PCCLB_P1_UNROLL 512
 #endif
 constexpr int kP1Unroll = PCCLB_P1_UNROLL;  // rows per unrolled block of the phase-1 loop
 
@@ -227,10 +230,14 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
       for (uint32_t s = 0; s < nst; ++s) {
         const uint32_t G = g + s, slot = G % C::STAGES;
         if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
-        // rows past the end of the tensor are zero-filled and still counted
+        // rows past the end of the tensor are zero-filled and still counted;
+        // stages taller than a TMA box (256 rows) take several boxes
+        constexpr int BR = R < 256 ? R : 256;
         mbar_expect_tx(&full[slot], L * R * 4);
-        tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)(row0 + (uint64_t)s * R),
-                   &full[slot]);
+#pragma unroll
+        for (int b = 0; b < R / BR; ++b)
+          tma_2d_g2s(stage + slot * C::STAGE_BYTES + b * BR * L * 4, map, (int)lane0,
+                     (int)(row0 + (uint64_t)s * R + b * BR), &full[slot]);
       }
     }
   } else {
@@ -638,7 +645,7 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       HashEntry &E = batch.e[slot];
       fill(k);
       const uint32_t mi = kMaxBatch + batch.nbig;  // phase-1 map slot
-      if (!E.map || !encode_map<kP1Lanes, kP1Rows>(&staging.host[mi], E.ptr, E.nbytes)) {
+      if (!E.map || !encode_map<kP1Lanes, (kP1Rows < 256 ? kP1Rows : 256)>(&staging.host[mi], E.ptr, E.nbytes)) {
         --slot;  // no tensor map: ordinary entry after all
         rest.push_back(k);
         continue;
