@@ -26,7 +26,7 @@
 // splits into lo' = (lo ^ w) * 435 mod 2^32, which depends on lo alone, and
 // hi' = 435 hi + umulhi(x, 435) + (x << 8) with x = lo ^ w, which is affine in
 // hi. So:
-//   phase 1 (one item per 64-lane quarter): run only the lo chain over the
+//   phase 1 (one item per kP1Lanes-lane slice, 32 lanes x 512-row stages): run only the lo chain over the
 //     whole entry (10.5 instead of 14.5 cycles per step) and publish lo at
 //     every kSegRows-row checkpoint;
 //   phase 2 (one item per segment and lane group, run by any free CTA as soon
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
     const uint32_t it = s_item;
     if (it >= items) break;
     if (it < n1) {
-      // phase 1: the lo chain of one 64-lane quarter of a big entry
+      // phase 1: the lo chain of one kP1Lanes-lane slice of a big entry
       const uint32_t e = it / P1, q = it % P1;
       const HashEntry E = b.e[e];
       const uint32_t lane0 = q * kP1Lanes;
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
       }
     } else {
       // phase 2: segment j of one 128-lane group of a big entry, once phase 1
-      // published the lo values that start it (two 64-lane quarters)
+      // published the lo values that start it (C::LANES / kP1Lanes slices)
       const uint32_t kk = it - n2;
       const uint32_t j = kk / nseg_items, r = kk % nseg_items, e = r / G, grp = r % G;
       const HashEntry E = b.e[e];
