@@ -78,7 +78,11 @@ constexpr int kIpcThreads = 512;
 constexpr uint64_t kQB = PCCLB_QB;  // elements per ready-flag block of the fused quantized steps
 // fused gather blocks: larger (fewer release fences; measured W=2: 64 Ki 1.92 ms, 256 Ki 1.80 ms)
 constexpr uint64_t kQF = 4 * kQB;
-constexpr int kQThreads = 256;
+#ifndef PCCLB_QTHREADS
+#define PCCLB_QTHREADS 256
+#endif
+constexpr int kQThreads = PCCLB_QTHREADS;
+constexpr int kQMinBlocks = 1024 / kQThreads;  // 64 registers per thread
 
 struct Signal {
   uint64_t arrive[kIpcMaxWorld];     // written by peer j: its latest barrier token
@@ -734,7 +738,7 @@ __device__ __forceinline__ void cta_loop16(uint64_t lo, uint64_t i0, uint64_t i1
 }
 
 template <int OP>
-__global__ void __launch_bounds__(kQThreads, 4) ipc_qstep_kernel(const __grid_constant__ QStepArgs a) {
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qstep_kernel(const __grid_constant__ QStepArgs a) {
   __shared__ uint32_t s_item, s_ok;
   const uint64_t nA = qblocks(a.tlo, a.tn), nB = qblocks(a.rlo, a.rn);
   uint64_t npos = 2 * nA;
@@ -887,7 +891,7 @@ struct QuantPushF {
   }
 };
 
-__global__ void __launch_bounds__(kQThreads, 4) ipc_qfinal_kernel(const __grid_constant__ QFinalArgs a) {
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(const __grid_constant__ QFinalArgs a) {
   __shared__ uint32_t s_item, s_ok;
   const uint32_t w = a.world, own = a.own;
   const uint64_t olo = a.lo[own], on = a.lo[own + 1] - olo;
