@@ -188,6 +188,9 @@ PCCLB_API volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r);
  * takes at most its share of the SM's CTA slots; with more engines than slots
  * the engine falls back to one barrier per ring step. */
 PCCLB_API int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots);
+/* Workspace bytes an n-element op needs at this world size (host-only, no
+ * GPU needed): the capacity_bytes to pass to pcclb_ring_create. 0 if invalid. */
+PCCLB_API uint64_t pcclb_ring_workspace_bytes(uint64_t n, uint32_t world, int dtype, int quantize);
 /* Element capacity for a dtype/quantize combination with this workspace. */
 PCCLB_API uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize);
 

@@ -1651,6 +1651,11 @@ int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle64) {
   return PCCLB_OK;
 }
 
+uint64_t pcclb_ring_workspace_bytes(uint64_t n, uint32_t world, int dtype, int quantize) {
+  if (world < 1 || world > (uint32_t)kIpcMaxWorld || !valid_dtype(dtype)) return 0;
+  return layout_for(n, world, dtype_size(dtype), quantize != 0).end;
+}
+
 int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots) {
   if (!r || slots < 1) return PCCLB_EINVAL;
   r->slots = slots;

@@ -124,12 +124,13 @@ class DeviceRing:
 
     @staticmethod
     def required_bytes(n: int, world: int, esz: int, quantize: bool) -> int:
-        """Workspace bytes for an n-element op (upper bound of the engine's layout)."""
-        nc = (n + world - 1) // world
-        need = 16384 + n * esz + 4 * nc * esz + 4096
-        if quantize:  # step codes, final codes, gathered codes + ready flags
-            need += 2 * world * (nc + 512) + 2 * world * (nc // 65536 + 3) * 8
-        return int(need * 1.02)
+        """Workspace bytes for an n-element op: the engine's own layout
+        (pcclb_ring_workspace_bytes, host-only)."""
+        code = 2 if esz == 8 else 1  # wire.py dtype codes: 1 f32, 2 f64
+        need = int(lib().pcclb_ring_workspace_bytes(n, world, code, int(quantize)))
+        if need == 0:
+            raise UsageError(f"no workspace layout for n={n}, world={world}")
+        return need + 4096
 
     def ensure_capacity(self, n: int, dtype: torch.dtype, quantize: bool) -> None:
         code = DTYPE_CODE[dtype]

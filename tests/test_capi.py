@@ -87,3 +87,23 @@ def test_sass_is_sm100a_and_uses_bulk_copies():
             assert "FFMA" not in f and "DFMA" not in f, name
             checked += 1
     assert checked >= 4
+
+
+def test_ring_workspace_bytes_host_only():
+    """pcclb_ring_workspace_bytes sizes the engine workspace without a GPU:
+    monotone in n, covers the backup copy, and the quantized layout (per-step
+    code buffers, gathered codes, ready flags) differs from the plain one."""
+    lib = _native.lib()
+    f = lib.pcclb_ring_workspace_bytes
+    assert f(100, 0, 1, 0) == 0 and f(100, 65, 1, 0) == 0 and f(100, 2, 7, 0) == 0
+    for w in (2, 3, 4, 8):
+        prev = 0
+        for n in (0, 1, 1000, 65536 * w + 5, 1 << 24):
+            plain, quant, f64 = f(n, w, 1, 0), f(n, w, 1, 1), f(n, w, 2, 0)
+            assert plain >= 16384 + 4 * n and f64 >= 16384 + 8 * n
+            assert quant >= 16384 + 4 * n + w * ((n + w - 1) // w)
+            assert plain >= prev
+            prev = plain
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
+
+    assert DeviceRing.required_bytes(1 << 20, 4, 4, True) >= f(1 << 20, 4, 1, 1)
