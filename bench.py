@@ -155,6 +155,8 @@ def dist_init(n: int):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(n)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available() and torch.cuda.device_count() > 0:
+        local %= torch.cuda.device_count()  # >1 rank per GPU only when oversubscribed (W=8 dry run on 4 GPUs)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
     torch.cuda.set_device(local)

@@ -31,7 +31,8 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
+    gpu = rank % torch.cuda.device_count()  # >1 rank per GPU only in the oversubscribed W=8 check
+    torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import ring as oring
     from paper_2505_14065_b200.collective import CollectiveAborted, UsageError
@@ -41,7 +42,7 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
 
     with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
         golden = json.load(f)
-    dev = torch.device("cuda", rank)
+    dev = torch.device("cuda", gpu)
     out: dict = {"rank": rank, "checks": [], "errors": []}
 
     def check(name, ok, detail=""):
