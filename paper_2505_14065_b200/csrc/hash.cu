@@ -58,7 +58,7 @@ constexpr int kHashMinBlocks = 12;
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 #ifndef PCCLB_SEGROWS
-#define PCCLB_SEGROWS 32768  // measured (one 1.05 GB entry): 4096 6.38 ms, 16384 6.06 / 5.74, 32768 5.69 ms
+#define PCCLB_SEGROWS 32768  // measured (one 1.05 GB entry): 4096 6.38 ms, 16384 6.06 / 5.74, 32768 5.69-5.71, 65536 5.76, 131072 5.91 ms
 #endif
 constexpr uint32_t kSegRows = PCCLB_SEGROWS;  // checkpoint spacing of the two-phase path (rows of 1 KiB)
 constexpr uint32_t kMaxBig = 16;     // big entries per launch
