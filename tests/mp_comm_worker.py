@@ -23,7 +23,8 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
+    gpu = rank % torch.cuda.device_count()  # oversubscribed (same-device IPC) when GPUs < world
+    torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import ring as oring
     from oracle import simplehash as osh
@@ -31,7 +32,7 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
     from paper_2505_14065_b200.communicator import Communicator, SyncStatus
     from paper_2505_14065_b200.sharedstate import DType, SharedStateEntry
 
-    dev = torch.device("cuda", rank)
+    dev = torch.device("cuda", gpu)
     out: dict = {"rank": rank, "checks": [], "errors": []}
 
     def check(name, ok, detail=""):

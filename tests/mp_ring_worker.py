@@ -211,8 +211,8 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             check("qedge: schedule mismatch rejected", rejected)
             check("qedge: schedule mismatch intact", buf.cpu().numpy().tobytes() == inputs[eng.position].tobytes())
             eng.close()
-        if "large" in scenarios:
-            n = (1 << 24) + 3
+        if "large" in scenarios or "large_small" in scenarios:
+            n = (1 << 24) + 3 if "large" in scenarios else (1 << 21) + 3
             for quant in (False, True):
                 inputs = [np.random.default_rng(70 + p).normal(0, 1, n).astype(np.float32) for p in range(world)]
                 buf = torch.from_numpy(inputs[ring.position].copy()).to(dev)

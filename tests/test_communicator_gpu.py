@@ -28,8 +28,9 @@ def _free_port() -> int:
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_communicator(world, tmp_path):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    # fewer GPUs than ranks: ranks share devices over same-device CUDA IPC
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
     cmd = [sys.executable, os.path.join(ROOT, "tests", "mp_comm_worker.py"), str(world), str(_free_port()), str(tmp_path)]
     proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert proc.returncode == 0, proc.stderr[-4000:]
