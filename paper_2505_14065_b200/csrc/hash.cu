@@ -21,21 +21,13 @@
 // mbarriers. Items are handed out by an atomic counter in LPT order (largest
 // entries first) -- list scheduling -- and the last group of an entry folds.
 //
-// Two-phase path for entries whose chain outlasts the rest of the batch
-// ("big" entries, e.g. config 4's 1.05 GB embedding and LM head). The FNV step
-// splits into lo' = (lo ^ w) * 435 mod 2^32, which depends on lo alone, and
-// hi' = 435 hi + umulhi(x, 435) + (x << 8) with x = lo ^ w, which is affine in
-// hi. So:
-//   phase 1 (one item per kP1Lanes-lane slice, 32 lanes x 512-row stages): run only the lo chain over the
-//     whole entry (10.5 instead of 14.5 cycles per step) and publish lo at
-//     every kSegRows-row checkpoint;
-//   phase 2 (one item per segment and lane group, run by any free CTA as soon
-//     as its checkpoint is published): rerun the full step over the segment
-//     from (lo = checkpoint, hi = 0), which leaves hi = A_j, the segment's
-//     additive term;
-//   combine (by the last finisher): hi = 435^m_j * hi + A_j over the segments,
-//     h = hi:lo_final, then the tail words and the tree fold.
-// Phase 2 reads the entry a second time, in parallel on otherwise idle SMs.
+// Big entries -- those whose 256 chains would outlast the HBM-bound time of
+// the whole call, e.g. config 4's 1.05 GB embedding and LM head -- go to a
+// second kernel launched concurrently on a side stream: loscan.cuh runs the
+// lo half of each chain as 32 bitsliced prefix scans (the lo step is a
+// T-function) instead of a serial 10.5-cycle-per-row chain, and derives the
+// affine hi half from the x values the scan leaves behind, so the entry is
+// read once and finished inside that kernel (lane states, tail words, fold).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -59,47 +51,34 @@ namespace pcclb {
 constexpr int kHashMinBlocks = 12;
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-#ifndef PCCLB_SEGROWS
-#define PCCLB_SEGROWS 32768  // measured (one 1.05 GB entry): 4096 6.38 ms, 16384 6.06 / 5.74, 32768 5.69-5.71, 65536 5.76, 131072 5.91 ms
-#endif
-constexpr uint32_t kSegRows = PCCLB_SEGROWS;  // checkpoint spacing of the two-phase path (rows of 1 KiB)
-constexpr uint32_t kMaxBig = 16;     // big entries per launch
+constexpr uint32_t kMaxBig = 16;     // big entries per call
 constexpr int kMaxBatch = 560;       // HashBatch must fit the 32 KiB kernel-parameter space
-// phase-1 items: 64 lanes per CTA and 256-row boxes, so each lo chain CTA keeps
-// ~2.7 us of TMA in flight (the lo chain consumes 512 B per ~10.5 cycles per
-// 128 lanes, more than one CTA's stream of 128-lane boxes sustains)
-#ifndef PCCLB_P1_LANES
-#define PCCLB_P1_LANES 32  // measured (one 1.05 GB entry): 64 lanes x 256 rows 6.06 ms, 32 x 512 5.74 ms
-#endif
-constexpr int kP1Lanes = PCCLB_P1_LANES;
-constexpr int kP1Rows = 256 * 64 / kP1Lanes;  // one 64 KiB stage
-constexpr int kP1Groups = 256 / kP1Lanes;
-#ifndef PCCLB_P1_UNROLL
-#define PCCLB_P1_UNROLL 512
-#endif
-constexpr int kP1Unroll = PCCLB_P1_UNROLL;  // rows per unrolled block of the phase-1 loop
+constexpr uint32_t kBigCtas = 256 / kLsLanes;  // loscan CTAs per big entry
 
 struct HashEntry {
   const uint8_t *ptr;
   uint64_t nbytes;
   uint64_t *out;
   const CUtensorMap *map;  // 2-D view [rounds x 256] u32, or null (direct loads)
-  const CUtensorMap *map1; // big entries: the same view with phase-1 boxes
-  uint32_t *aux;           // big entries: [nseg x 256] checkpoints, [256] final lo, [nseg x 256] A
-  uint32_t nseg;           // big entries: number of kSegRows segments
-  uint32_t pad;
 };
 
-// Entries [0, nbig) are big (two-phase); item space:
-//   [0, n1 = nbig*P1)                   phase-1 lo chains (P1 = kP1Groups)
-//   [n1, n2 = n1 + (count-nbig)*G)      ordinary entries' lane groups
-//   [n2, n2 + segmax*nbig*G)            phase-2 segments, segment-major
+// ordinary entries: item = one lane group of one entry, entries in LPT order
 struct HashBatch {
   uint32_t count;
-  uint32_t nbig;
-  uint32_t segmax;
   uint32_t pad;
   HashEntry e[kMaxBatch];
+};
+
+// big entries: kBigCtas loscan CTAs each
+struct BigEntry {
+  CUtensorMap map;  // 4-D view [segment][i][t][lane] (loscan.cuh)
+  const uint8_t *ptr;
+  uint64_t nbytes;
+  uint64_t *out;
+  uint64_t pad;
+};
+struct BigBatch {
+  BigEntry e[kMaxBig];
 };
 
 // One FNV-1a-64 step h = (h ^ w) * P on the split state (lo, hi).
@@ -118,23 +97,11 @@ struct Fnv {
     // explicit mad so the compiler cannot re-associate x-terms onto the hi chain
     asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hi) : "r"(hi), "r"(add));
   }
-  // phase 1 of the two-phase path: the lo chain alone
-  __device__ __forceinline__ void step_lo(uint32_t w) { lo = (lo ^ w) * 435u; }
 };
 __device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint32_t w) {
   return (h ^ (uint64_t)w) * kFnvPrime;
 }
 __device__ __forceinline__ uint64_t rotl27(uint64_t v) { return (v << 27) | (v >> 37); }
-// 435^m mod 2^32
-__device__ __forceinline__ uint32_t pow435(uint32_t m) {
-  uint32_t r = 1, b = 435u;
-  while (m) {
-    if (m & 1u) r *= b;
-    b *= b;
-    m >>= 1;
-  }
-  return r;
-}
 
 // little-endian u32 at an arbitrary byte address (zero beyond `avail` bytes)
 __device__ __forceinline__ uint32_t load_word_any(const uint8_t *p, uint32_t avail) {
@@ -157,30 +124,33 @@ struct HashCfg {
   static constexpr int GROUPS = 256 / LANES;
   static constexpr int STAGE_BYTES = ROWS * LANES * 4;
   static constexpr int SMEM = STAGE_BYTES * STAGES;
-  static_assert(kSegRows % ROWS == 0, "segments are whole stages");
 };
 // Measured (config-4 layout / one 1.05 GB entry / 64 x 64 MiB, full steps,
 // tools/hash_variants.py): <128,128,3> 8.5 ms / 131 GB/s / 7.1 TB/s;
 // <64,128,4> 8.2 ms / 128 GB/s / 4.0 TB/s (64 lanes per SM starve HBM);
 // <128,96,4> 9.0 ms; <128,64,3> without the producer warp 10.6 ms. Deep
 // stages keep ~2 us of TMA lookahead per CTA and amortise the handshakes.
-using HashC = HashCfg<128, 128, 3>;
+#ifndef PCCLB_HASH_ROWS
+#define PCCLB_HASH_ROWS 64
+#endif
+#ifndef PCCLB_HASH_STAGES
+#define PCCLB_HASH_STAGES 3
+#endif
+#ifndef PCCLB_HASH_LANES
+#define PCCLB_HASH_LANES 128
+#endif
+using HashC = HashCfg<PCCLB_HASH_LANES, PCCLB_HASH_ROWS, PCCLB_HASH_STAGES>;
 
-// Rows [row0, row0 + nrows) of lanes [lane0, lane0 + L) through the TMA ring
-// (boxes of L lanes x R rows); h is the lane's state (threads < L). The
-// producer thread (thread C::LANES) issues a stage into slot g % STAGES once
-// the C::WARPS lane warps released it (empty[slot]); `g` numbers the stages of
-// the whole launch, so the mbarrier phase parity is (g / STAGES) & 1. Lane
-// warps beyond L only keep the ring protocol. LO_ONLY: step the lo chain only
-// and, every kSegRows rows (row0 = 0), store the lo value that starts the
-// segment to ck[seg * 256 + lane] and count each writing warp in *progress.
-template <class C, int L, int R, bool LO_ONLY>
-__device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t lane0, uint64_t row0,
-                                             uint64_t nrows, uint64_t h, uint8_t *stage,
-                                             uint64_t *full, uint64_t *empty, uint32_t &g,
-                                             uint32_t *ck, uint32_t *progress) {
-  static_assert(L * R * 4 <= C::STAGE_BYTES && kSegRows % R == 0, "box fits a slot");
-  static_assert(L == C::LANES || L + 32 <= C::LANES, "narrow boxes start at warp 1");
+// Rows [0, nrows) of lanes [lane0, lane0 + C::LANES) through the TMA ring
+// (boxes of C::LANES lanes x C::ROWS rows); h is the lane's state (threads <
+// C::LANES). The producer thread (thread C::LANES) issues a stage into slot
+// g % STAGES once the C::WARPS lane warps released it (empty[slot]); `g`
+// numbers the stages of the whole launch, so the mbarrier phase parity is
+// (g / STAGES) & 1.
+template <class C>
+__device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t lane0, uint64_t nrows, uint64_t h,
+                                             uint8_t *stage, uint64_t *full, uint64_t *empty, uint32_t &g) {
+  constexpr int L = C::LANES, R = C::ROWS;
   const int tid = threadIdx.x;
   const uint32_t nst = (uint32_t)((nrows + R - 1) / R);
   if (tid >= C::LANES) {
@@ -189,69 +159,30 @@ __device__ __forceinline__ uint64_t run_rows(const CUtensorMap *map, uint32_t la
       for (uint32_t s = 0; s < nst; ++s) {
         const uint32_t G = g + s, slot = G % C::STAGES;
         if (G >= (uint32_t)C::STAGES) mbar_wait(&empty[slot], ((G / C::STAGES) - 1) & 1u);
-        // rows past the end of the tensor are zero-filled and still counted;
-        // stages taller than a TMA box (256 rows) take several boxes
-        constexpr int BR = R < 256 ? R : 256;
+        // rows past the end of the tensor are zero-filled and still counted
         mbar_expect_tx(&full[slot], L * R * 4);
-#pragma unroll
-        for (int b = 0; b < R / BR; ++b)
-          tma_2d_g2s(stage + slot * C::STAGE_BYTES + b * BR * L * 4, map, (int)lane0,
-                     (int)(row0 + (uint64_t)s * R + b * BR), &full[slot]);
+        tma_2d_g2s(stage + slot * C::STAGE_BYTES, map, (int)lane0, (int)((uint64_t)s * R), &full[slot]);
       }
     }
   } else {
-    // narrower boxes run on warps 1.. (warp 0 shares its SMSP with the producer)
-    constexpr int off = (L < C::LANES) ? 32 : 0;
-    const int t = tid - off;
-    const bool active = t >= 0 && t < L;
+    const int t = tid;
     for (uint32_t s = 0; s < nst; ++s) {
       const uint32_t G = g + s, slot = G % C::STAGES;
-      if constexpr (LO_ONLY) {
-        if (active && (s * R) % kSegRows == 0) {
-          ck[(s * R / kSegRows) * 256 + lane0 + t] = (uint32_t)h;
-          __syncwarp();
-          if ((tid & 31) == 0) {
-            __threadfence();  // ~3% of phase 1 (measured against an unordered count)
-            atomicAdd(progress, 1u);
-          }
-        }
-      }
       mbar_wait(&full[slot], (G / C::STAGES) & 1u);
-      if (active) {
-        // the state is unpacked per stage: it keeps the compiler from
-        // rescheduling the hi chain across stages (measured 35% slower)
-        Fnv f(h);
-        const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + t;
-        const uint64_t left = nrows - (uint64_t)s * R;
-        if (LO_ONLY && kP1Unroll < R && left >= (uint64_t)R) {
-          // lo chain in kP1Unroll-row unrolled blocks (smaller code body)
-          constexpr int UB = kP1Unroll < R ? kP1Unroll : R;
-#pragma unroll 1
-          for (int r0 = 0; r0 < R; r0 += UB) {
+      // the state is unpacked per stage: it keeps the compiler from
+      // rescheduling the hi chain across stages (measured 35% slower)
+      Fnv f(h);
+      const uint32_t *wds = reinterpret_cast<const uint32_t *>(stage + slot * C::STAGE_BYTES) + t;
+      const uint64_t left = nrows - (uint64_t)s * R;
+      if (left >= (uint64_t)R) {
+        // fully unrolled: the shared-memory loads are hoisted ahead of the chain
 #pragma unroll
-            for (int r = 0; r < UB; ++r) f.step_lo(wds[(r0 + r) * L]);
-          }
-        } else if (left >= (uint64_t)R) {
-          // fully unrolled: the shared-memory loads are hoisted ahead of the chain
-          // (measured best for both forms, e.g. phase 1: 6.24 ms at 256 vs 6.8 at 32)
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            if constexpr (LO_ONLY)
-              f.step_lo(wds[r * L]);
-            else
-              f.step(wds[r * L]);
-          }
-        } else {
-          const int nr = (int)left;
-          for (int r = 0; r < nr; ++r) {
-            if constexpr (LO_ONLY)
-              f.step_lo(wds[r * L]);
-            else
-              f.step(wds[r * L]);
-          }
-        }
-        h = f.value();
+        for (int r = 0; r < R; ++r) f.step(wds[r * L]);
+      } else {
+        const int nr = (int)left;
+        for (int r = 0; r < nr; ++r) f.step(wds[r * L]);
       }
+      h = f.value();
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
     }
@@ -282,8 +213,7 @@ __device__ __forceinline__ uint64_t hash_group(const uint8_t *p, uint64_t nbytes
   const uint32_t lane = lane0 + threadIdx.x;
   const uint64_t rounds = nbytes >> 10;
   if (rounds > 0 && map != nullptr) {
-    h = run_rows<C, C::LANES, C::ROWS, false>(map, lane0, 0, rounds, h, stage, bars, bars + C::STAGES, g,
-                                              nullptr, nullptr);
+    h = run_rows<C>(map, lane0, rounds, h, stage, bars, bars + C::STAGES, g);
   } else if (threadIdx.x < C::LANES) {
     for (uint64_t r = 0; r < rounds; ++r) h = fnv_step(h, load_word_any(p + ((r << 8) + lane) * 4, 4));
   }
@@ -329,102 +259,98 @@ __device__ __forceinline__ bool last_part(uint32_t *counter, uint32_t parts, uin
   return last;
 }
 
-// Combine of the two-phase path: hi over the segments, the tail, the fold.
-__device__ __forceinline__ void big_combine(const HashEntry &E, uint64_t *lane_s) {
-  const uint64_t rounds = E.nbytes >> 10;
-  const uint32_t *lofinal = E.aux + (size_t)E.nseg * 256;
-  const uint32_t *A = lofinal + 256;
-  const uint32_t pw = pow435(kSegRows);
-  for (int lane = threadIdx.x; lane < 256; lane += blockDim.x) {
-    uint32_t hi = (uint32_t)(kFnvOffset >> 32);
-#pragma unroll 8
-    for (uint32_t j = 0; j < E.nseg; ++j) {
-      const uint64_t m = min((uint64_t)kSegRows, rounds - (uint64_t)j * kSegRows);
-      hi = (m == kSegRows ? pw : pow435((uint32_t)m)) * hi + __ldcg(&A[(size_t)j * 256 + lane]);
-    }
-    const uint64_t h = ((uint64_t)hi << 32) | __ldcg(&lofinal[lane]);
-    lane_s[lane] = tail_steps(h, E.ptr, E.nbytes, lane);
-  }
-  const uint64_t root = tree_fold(lane_s);
-  if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+#ifdef PCCLB_HASH_TRACE
+// debug timeline: per CTA {kernel, smid, start, end} (globaltimer ns)
+__device__ unsigned long long g_trace[8192][4];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TRACE_BEGIN() const uint64_t tr_t0 = gtimer()
+#define TRACE_END(kind)                                             \
+  if (threadIdx.x == 0) {                                           \
+    const uint32_t i = atomicAdd(&g_trace_n, 1u);                   \
+    if (i < 8192) {                                                 \
+      g_trace[i][0] = kind;                                         \
+      g_trace[i][1] = smid();                                       \
+      g_trace[i][2] = tr_t0;                                        \
+      g_trace[i][3] = gtimer();                                     \
+    }                                                               \
+  }
+#else
+#define TRACE_BEGIN()
+#define TRACE_END(kind)
+#endif
 
-// One launch for a batch of entries. Scratch: lanes[count x 256] (ordinary
-// entries' lane values), cnt = [count arrivals | item counter | nbig*G phase-1
-// progress counters | nbig completion counters].
+// One launch for a batch of ordinary entries. Scratch: lanes[count x 256]
+// (lane values), cnt = [count arrivals | item counter].
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
     simplehash_batch_kernel(const __grid_constant__ HashBatch b, uint64_t *lanes, uint32_t *cnt) {
+  TRACE_BEGIN();
   extern __shared__ __align__(1024) uint8_t stage[];
   __shared__ __align__(8) uint64_t bars[2 * C::STAGES];
   __shared__ uint64_t lane_s[256];
   __shared__ uint32_t s_flag, s_item;
   init_bars<C>(bars);
-  constexpr uint32_t G = C::GROUPS, P1 = kP1Groups;
+  constexpr uint32_t G = C::GROUPS;
   uint32_t *arrived = cnt;
   uint32_t *next = cnt + b.count;
-  uint32_t *progress = next + 1;
-  uint32_t *bigdone = progress + b.nbig * P1;
-  const uint32_t n1 = b.nbig * P1, n2 = n1 + (b.count - b.nbig) * G, nseg_items = b.nbig * G;
-  const uint32_t items = n2 + b.segmax * nseg_items;
+  const uint32_t items = b.count * G;
   uint32_t g = 0;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(next, 1u);
     __syncthreads();
     const uint32_t it = s_item;
     if (it >= items) break;
-    if (it < n1) {
-      // phase 1: the lo chain of one kP1Lanes-lane slice of a big entry
-      const uint32_t e = it / P1, q = it % P1;
-      const HashEntry E = b.e[e];
-      const uint32_t lane0 = q * kP1Lanes;
-      const uint64_t h = run_rows<C, kP1Lanes, kP1Rows, true>(E.map1, lane0, 0, E.nbytes >> 10, kFnvOffset,
-                                                              stage, bars, bars + C::STAGES, g, E.aux,
-                                                              &progress[it]);
-      if (threadIdx.x >= 32 && threadIdx.x < 32 + kP1Lanes)  // run_rows' lane offset
-        E.aux[(size_t)E.nseg * 256 + lane0 + threadIdx.x - 32] = (uint32_t)h;
-      if (last_part(&bigdone[e], P1 + G * E.nseg, &s_flag)) big_combine(E, lane_s);
-    } else if (it < n2) {
-      // an ordinary entry's lane group; the last group of the entry folds
-      const uint32_t e = b.nbig + (it - n1) / G, grp = (it - n1) % G;
-      const HashEntry E = b.e[e];
-      const uint32_t lane0 = grp * C::LANES;
-      const uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, g);
-      if (threadIdx.x < C::LANES) lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
-      if (last_part(&arrived[e], G, &s_flag)) {
-        for (int j = threadIdx.x; j < 256; j += blockDim.x)
-          lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
-        const uint64_t root = tree_fold(lane_s);
-        if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
-      }
-    } else {
-      // phase 2: segment j of one 128-lane group of a big entry, once phase 1
-      // published the lo values that start it (C::LANES / kP1Lanes slices)
-      const uint32_t kk = it - n2;
-      const uint32_t j = kk / nseg_items, r = kk % nseg_items, e = r / G, grp = r % G;
-      const HashEntry E = b.e[e];
-      if (j < E.nseg) {
-        if (threadIdx.x == 0) {
-          constexpr uint32_t per = C::LANES / kP1Lanes, wq = kP1Lanes / 32;
-          for (uint32_t q = 0; q < per; ++q)
-            while (ld_acquire(&progress[e * P1 + grp * per + q]) < (j + 1) * wq) __nanosleep(256);
-        }
-        __syncthreads();
-        const uint32_t lane0 = grp * C::LANES;
-        const uint64_t rounds = E.nbytes >> 10;
-        const uint64_t row0 = (uint64_t)j * kSegRows;
-        const uint32_t lo0 =
-            threadIdx.x < C::LANES ? __ldcg(&E.aux[(size_t)j * 256 + lane0 + threadIdx.x]) : 0u;
-        const uint64_t h = run_rows<C, C::LANES, C::ROWS, false>(
-            E.map, lane0, row0, min((uint64_t)kSegRows, rounds - row0), (uint64_t)lo0, stage, bars,
-            bars + C::STAGES, g, nullptr, nullptr);
-        if (threadIdx.x < C::LANES)
-          E.aux[(size_t)(E.nseg + 1) * 256 + (size_t)j * 256 + lane0 + threadIdx.x] = (uint32_t)(h >> 32);
-        if (last_part(&bigdone[e], P1 + G * E.nseg, &s_flag)) big_combine(E, lane_s);
-      }
+    // an entry's lane group; the last group of the entry folds
+    const uint32_t e = it / G, grp = it % G;
+    const HashEntry E = b.e[e];
+    const uint32_t lane0 = grp * C::LANES;
+    const uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, g);
+    if (threadIdx.x < C::LANES) lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
+    if (last_part(&arrived[e], G, &s_flag)) {
+      for (int j = threadIdx.x; j < 256; j += blockDim.x) lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
+      const uint64_t root = tree_fold(lane_s);
+      if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
     }
     __syncthreads();
   }
+  TRACE_END(1);
+}
+
+// Big entries: kBigCtas CTAs per entry, each the whole chains of kLsLanes
+// lanes (loscan.cuh), then the tail words; the last CTA of an entry folds.
+// Scratch: lanes[kMaxBig x 256], done[kMaxBig].
+__global__ void __launch_bounds__(kLsThreads, 1)
+    simplehash_big_kernel(const __grid_constant__ BigBatch bb, uint64_t *lanes, uint32_t *done) {
+  TRACE_BEGIN();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t s_flag;
+  auto *sh = reinterpret_cast<LsShared *>(smem + kLsStageBytes * kLsStages);
+  const uint32_t e = blockIdx.x / kBigCtas, q = blockIdx.x % kBigCtas;
+  const BigEntry &E = bb.e[e];
+  const uint32_t lane0 = q * kLsLanes;
+  loscan_cta(&E.map, E.ptr, E.nbytes >> 10, lane0, smem, sh);
+  if (threadIdx.x < kLsLanes) {
+    const uint32_t lane = lane0 + threadIdx.x;
+    const uint64_t h = ((uint64_t)sh->final_hi[threadIdx.x] << 32) | sh->final_lo[threadIdx.x];
+    lanes[(uint64_t)e * 256 + lane] = tail_steps(h, E.ptr, E.nbytes, lane);
+  }
+  if (last_part(&done[e], kBigCtas, &s_flag)) {
+    uint64_t *lane_s = reinterpret_cast<uint64_t *>(smem);  // the stage area is free now
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);
+    const uint64_t root = tree_fold(lane_s);
+    if (threadIdx.x == 0) *E.out = root ^ E.nbytes;
+  }
+  TRACE_END(2);
 }
 
 // streaming update of one segment: grid = GROUPS CTAs, lane state in/out
@@ -452,10 +378,10 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *out = root ^ total;
 }
 
-// PCCLB_HASH_TWO_PHASE=0 disables the two-phase path (measurements, tests)
-static bool two_phase_enabled() {
+// PCCLB_HASH_BIG=0 keeps every entry on the batch kernel (measurements, tests)
+static bool big_path_enabled() {
   static bool on = [] {
-    const char *e = getenv("PCCLB_HASH_TWO_PHASE");
+    const char *e = getenv("PCCLB_HASH_BIG");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -514,14 +440,64 @@ static int prepare_hash_kernels() {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, HashC::SMEM));
   PCCLB_CUDA(cudaFuncSetAttribute(simplehash_update_kernel<HashC>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, HashC::SMEM));
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLsSmem));
+  // the batch and big-entry kernels share SMs: both ask for the full shared
+  // memory carveout, so an SM configured for one has room for the other
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_batch_kernel<HashC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+  PCCLB_CUDA(cudaFuncSetAttribute(simplehash_big_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
   if (dev >= 0 && dev < 64) done[dev] = true;
   return PCCLB_OK;
 }
 
 // Big entries: those whose full-step chain (~139 GB/s) would outlast the
-// HBM-bound time of the whole call (total bytes at ~6 TB/s), at least 64 MiB.
-static bool is_big(uint64_t nbytes, uint64_t total) {
-  return two_phase_enabled() && nbytes >= (64ull << 20) && nbytes * 40 > total;
+// HBM-bound time of the whole call (total bytes at ~6 TB/s), at least 64 MiB,
+// with a 16-byte aligned base (TMA).
+static bool is_big(const void *p, uint64_t nbytes, uint64_t total) {
+  return big_path_enabled() && nbytes >= (64ull << 20) && nbytes * 40 > total &&
+         (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (nbytes >> 10) < (1ull << 31);
+}
+
+// 4-D view of a big entry for loscan.cuh: dims {256 lanes, 32 t, 32 i, whole
+// 1024-row segments}, strides {4 B, 32 KiB, 1 KiB, 1 MiB}
+static bool encode_big_map(CUtensorMap *m, const void *p, uint64_t nbytes) {
+  const uint64_t nseg = nbytes >> 20;
+  auto fn = encode_fn();
+  if (!fn || nseg == 0) return false;
+  cuuint64_t dims[4] = {256, 32, 32, nseg};
+  cuuint64_t strides[3] = {32768, 1024, 1ull << 20};
+  cuuint32_t box[4] = {(cuuint32_t)kLsLanes, 32, 32, (cuuint32_t)kLsWarps};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void *>(p), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// side stream + fork/join events of the calling host thread (big entries run
+// beside the batch kernel)
+struct SideStream {
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~SideStream() {
+    // process teardown: the context may already be gone, errors are ignored
+    if (s) cudaStreamDestroy(s);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
+};
+
+static int side_stream(SideStream &ss) {
+  int dev = 0;
+  PCCLB_CUDA(cudaGetDevice(&dev));
+  if (ss.s && ss.dev == dev) return PCCLB_OK;
+  ss.dev = dev;
+  PCCLB_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+  PCCLB_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+  PCCLB_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  return PCCLB_OK;
 }
 
 // order: entry indices, largest first
@@ -537,36 +513,61 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
   const uint32_t slots = (uint32_t)(sm_count() * occ);
   uint64_t total = 0;
   for (uint32_t i = 0; i < count; ++i) total += h_nbytes[i];
-  // per-call device scratch: lane values, counters, tensor maps, big-entry aux
-  const uint32_t m_max = std::min<uint32_t>(kMaxBatch, count);
-  const size_t lanes_bytes = (size_t)m_max * 256 * sizeof(uint64_t);
-  const size_t cnt_words = (size_t)m_max + 1 + kMaxBig * (kP1Groups + 1);
-  const size_t cnt_bytes = (cnt_words * sizeof(uint32_t) + 127) & ~size_t(127);
-  const size_t map_bytes = ((size_t)kMaxBatch + kMaxBig) * sizeof(CUtensorMap);
-  size_t aux_bytes = 0;
-  for (uint32_t i = 0, nb = 0; i < count && nb < kMaxBig; ++i) {
-    const uint64_t n = h_nbytes[order[i]];
-    if (!is_big(n, total)) continue;
-    const uint64_t nseg = ((n >> 10) + kSegRows - 1) / kSegRows;
-    aux_bytes += (2 * nseg + 1) * 256 * sizeof(uint32_t);
-    ++nb;
+  // big entries (largest first) go to the loscan kernel, the rest to batches
+  static thread_local BigBatch big;
+  std::vector<uint32_t> rest;
+  uint32_t nbig = 0;
+  for (uint32_t k : order) {
+    if (nbig < kMaxBig && is_big(h_ptrs[k], h_nbytes[k], total) &&
+        encode_big_map(&big.e[nbig].map, h_ptrs[k], h_nbytes[k])) {
+      big.e[nbig].ptr = static_cast<const uint8_t *>(h_ptrs[k]);
+      big.e[nbig].nbytes = h_nbytes[k];
+      big.e[nbig].out = d_out + k;
+      big.e[nbig].pad = 0;
+      ++nbig;
+    } else {
+      rest.push_back(k);
+    }
   }
+  // per-call device scratch: lane values, counters, tensor maps
+  const uint32_t m_max = std::min<uint32_t>(kMaxBatch, (uint32_t)rest.size());
+  const size_t lanes_bytes = ((size_t)m_max + nbig) * 256 * sizeof(uint64_t);
+  const size_t cnt_words = (size_t)m_max + 1 + nbig;
+  const size_t cnt_bytes = (cnt_words * sizeof(uint32_t) + 127) & ~size_t(127);
+  const size_t map_bytes = (size_t)kMaxBatch * sizeof(CUtensorMap);
   char *scratch = nullptr;
-  PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch),
-                             lanes_bytes + cnt_bytes + map_bytes + aux_bytes, s));
+  PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), lanes_bytes + cnt_bytes + map_bytes, s));
   uint64_t *lanes = reinterpret_cast<uint64_t *>(scratch);
+  uint64_t *big_lanes = lanes + (size_t)m_max * 256;
   uint32_t *cnt = reinterpret_cast<uint32_t *>(scratch + lanes_bytes);
+  uint32_t *big_done = cnt + m_max + 1;
   CUtensorMap *d_maps = reinterpret_cast<CUtensorMap *>(scratch + lanes_bytes + cnt_bytes);
-  uint32_t *aux = reinterpret_cast<uint32_t *>(scratch + lanes_bytes + cnt_bytes + map_bytes);
   static thread_local HashBatch batch;
   static thread_local MapStaging staging;
+  static thread_local SideStream side;
   int rc = PCCLB_OK;
-  bool first = true;  // big entries are only taken in the first launch
-  for (uint32_t base = 0; base < count && rc == PCCLB_OK; base += kMaxBatch) {
-    const uint32_t m = std::min<uint32_t>(kMaxBatch, count - base);
+  bool forked = false;
+  cudaError_t e = cudaMemsetAsync(cnt, 0, cnt_words * sizeof(uint32_t), s);
+  if (e != cudaSuccess) rc = cuda_status(e);
+#ifndef PCCLB_BIG_AFTER
+  if (rc == PCCLB_OK && nbig) {
+    rc = side_stream(side);
+    if (rc == PCCLB_OK) {
+      e = cudaEventRecord(side.fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side.s, side.fork, 0);
+      if (e == cudaSuccess) {
+        forked = true;
+        simplehash_big_kernel<<<nbig * kBigCtas, kLsThreads, kLsSmem, side.s>>>(big, big_lanes, big_done);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) rc = cuda_status(e);
+    }
+  }
+#endif
+  for (uint32_t base = 0; base < (uint32_t)rest.size() && rc == PCCLB_OK; base += kMaxBatch) {
+    const uint32_t m = std::min<uint32_t>(kMaxBatch, (uint32_t)rest.size() - base);
     if (!staging.host) {
-      cudaError_t e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * (kMaxBatch + kMaxBig),
-                                    cudaHostAllocDefault);
+      e = cudaHostAlloc(&staging.host, sizeof(CUtensorMap) * kMaxBatch, cudaHostAllocDefault);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&staging.done, cudaEventDisableTiming);
       if (e != cudaSuccess) {
         rc = cuda_status(e);
@@ -576,69 +577,54 @@ static int launch_batches(const std::vector<uint32_t> &order, const void *const 
       cudaEventSynchronize(staging.done);  // previous upload out of the staging area
     }
     batch.count = m;
-    batch.nbig = 0;
-    batch.segmax = 0;
-    uint32_t *aux_next = aux;
-    uint32_t slot = 0;
-    auto fill = [&](uint32_t k) {
-      HashEntry &E = batch.e[slot];
+    batch.pad = 0;
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint32_t k = rest[base + i];
+      HashEntry &E = batch.e[i];
       E.ptr = static_cast<const uint8_t *>(h_ptrs[k]);
       E.nbytes = h_nbytes[k];
       E.out = d_out + k;
-      E.map = encode_map<C::LANES, C::ROWS>(&staging.host[slot], E.ptr, E.nbytes) ? d_maps + slot : nullptr;
-      E.map1 = nullptr;
-      E.aux = nullptr;
-      E.nseg = 0;
-      E.pad = 0;
-      ++slot;
-      return E;
-    };
-    // big entries first (slots [0, nbig)), then the others in LPT order
-    std::vector<uint32_t> rest;
-    for (uint32_t i = 0; i < m; ++i) {
-      const uint32_t k = order[base + i];
-      if (!(first && batch.nbig < kMaxBig && is_big(h_nbytes[k], total))) {
-        rest.push_back(k);
-        continue;
-      }
-      HashEntry &E = batch.e[slot];
-      fill(k);
-      const uint32_t mi = kMaxBatch + batch.nbig;  // phase-1 map slot
-      if (!E.map || !encode_map<kP1Lanes, (kP1Rows < 256 ? kP1Rows : 256)>(&staging.host[mi], E.ptr, E.nbytes)) {
-        --slot;  // no tensor map: ordinary entry after all
-        rest.push_back(k);
-        continue;
-      }
-      E.map1 = d_maps + mi;
-      E.nseg = (uint32_t)(((E.nbytes >> 10) + kSegRows - 1) / kSegRows);
-      E.aux = aux_next;
-      aux_next += (size_t)(2 * E.nseg + 1) * 256;
-      batch.segmax = std::max(batch.segmax, E.nseg);
-      ++batch.nbig;
+      E.map = encode_map<C::LANES, C::ROWS>(&staging.host[i], E.ptr, E.nbytes) ? d_maps + i : nullptr;
     }
-    std::stable_sort(rest.begin(), rest.end(),
-                     [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
-    for (uint32_t k : rest) fill(k);
-    first = false;
-    cudaError_t e =
-        cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && batch.nbig)
-      e = cudaMemcpyAsync(d_maps + kMaxBatch, staging.host + kMaxBatch, sizeof(CUtensorMap) * batch.nbig,
-                          cudaMemcpyHostToDevice, s);
+    e = cudaMemcpyAsync(d_maps, staging.host, sizeof(CUtensorMap) * m, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaEventRecord(staging.done, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, cnt_words * sizeof(uint32_t), s);
+    if (e == cudaSuccess && base > 0) e = cudaMemsetAsync(cnt, 0, ((size_t)m_max + 1) * sizeof(uint32_t), s);
     if (e != cudaSuccess) {
       rc = cuda_status(e);
       break;
     }
-    const uint64_t items = (uint64_t)batch.nbig * kP1Groups + (uint64_t)(m - batch.nbig) * C::GROUPS +
-                           (uint64_t)batch.segmax * batch.nbig * C::GROUPS;
-    const unsigned grid = (unsigned)std::min<uint64_t>(items, slots);
+    const uint64_t items = (uint64_t)m * C::GROUPS;
+    // beside the big-entry kernel: one batch CTA shares each SM with a loscan
+    // CTA (both ask for the full carveout and fit together), the others wait
+    // for SMs the loscan CTAs leave -- one extra CTA per SM for those
+    // (config 4: 3.07 ms at occupancy, 3.03 ms with the extra wave)
+    const unsigned grid = (unsigned)std::min<uint64_t>(items, nbig ? slots + (uint64_t)sm_count() : slots);
     simplehash_batch_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(batch, lanes, cnt);
     e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_status(e);
   }
-  cudaError_t e = cudaFreeAsync(scratch, s);
+#ifdef PCCLB_BIG_AFTER
+  if (rc == PCCLB_OK && nbig) {
+    rc = side_stream(side);
+    if (rc == PCCLB_OK) {
+      e = cudaEventRecord(side.fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side.s, side.fork, 0);
+      if (e == cudaSuccess) {
+        forked = true;
+        simplehash_big_kernel<<<nbig * kBigCtas, kLsThreads, kLsSmem, side.s>>>(big, big_lanes, big_done);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) rc = cuda_status(e);
+    }
+  }
+#endif
+  if (forked) {
+    // join even after an error, so the scratch is not freed under the big kernel
+    e = cudaEventRecord(side.join, side.s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, side.join, 0);
+    if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
+  }
+  e = cudaFreeAsync(scratch, s);
   if (rc == PCCLB_OK && e != cudaSuccess) rc = cuda_status(e);
   return rc;
 }
@@ -675,6 +661,22 @@ int pcclb_simplehash_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, 
                    [&](uint32_t a, uint32_t b) { return h_nbytes[a] > h_nbytes[b]; });
   return launch_batches(order, h_ptrs, h_nbytes, d_out, as_stream(stream));
 }
+
+#ifdef PCCLB_HASH_TRACE
+__attribute__((visibility("default"))) int pcclb_debug_hash_trace(unsigned long long *host, int max, int reset) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
+  if (n > 8192) n = 8192;
+  if ((int)n > max) n = (unsigned)max;
+  cudaMemcpyFromSymbol(host, g_trace, (size_t)n * 32);
+  if (reset) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  }
+  return (int)n;
+}
+#endif
 
 int pcclb_simplehash(const void *d_data, uint64_t nbytes, uint64_t *d_out, void *stream) {
   return pcclb_simplehash_multi(&d_data, &nbytes, 1, d_out, stream);

@@ -45,10 +45,13 @@ namespace pcclb {
 
 constexpr int kLsLanes = 4;  // lanes per CTA: 16 B of every 1 KiB row
 #ifndef PCCLB_LS_WARPS
-#define PCCLB_LS_WARPS 4
+#define PCCLB_LS_WARPS 5
 #endif
 constexpr int kLsWarps = PCCLB_LS_WARPS;  // warps (1024-row segments per block) per lane
-constexpr int kLsStages = 2;
+#ifndef PCCLB_LS_STAGES
+#define PCCLB_LS_STAGES 1
+#endif
+constexpr int kLsStages = PCCLB_LS_STAGES;
 constexpr int kLsThreads = (kLsLanes * kLsWarps + 1) * 32;  // + the TMA producer warp
 constexpr uint32_t kLsBlockRows = 1024u * kLsWarps;
 constexpr uint32_t kLsStageBytes = kLsBlockRows * kLsLanes * 4;
@@ -104,14 +107,14 @@ __device__ __forceinline__ void st_volatile_shared2(uint2 *p, uint32_t x, uint32
 }
 // spins until p->y == tag (warp-uniform address), returns p->x
 __device__ __forceinline__ uint32_t ls_await(const uint2 *p, uint32_t tag) {
-  uint32_t x, y;
+  uint32_t x;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
+      "{\n\t.reg .pred p;\n\t.reg .b32 y;\n"
       "LS_WAIT_%=:\n\t"
-      "ld.volatile.shared.v2.u32 {%0, %1}, [%2];\n\t"
-      "setp.ne.u32 p, %1, %3;\n\t"
+      "ld.volatile.shared.v2.u32 {%0, y}, [%1];\n\t"
+      "setp.ne.u32 p, y, %2;\n\t"
       "@p bra LS_WAIT_%=;\n}"
-      : "=r"(x), "=r"(y)
+      : "=r"(x)
       : "r"(smem_u32(p)), "r"(tag)
       : "memory");
   return x;
@@ -156,6 +159,7 @@ __device__ __forceinline__ void ls_planes(uint32_t (&X)[32], uint32_t valid, Sta
     publish(b, sb ^ (uint32_t)__popc(bal));
     const uint32_t run = (sb ^ (uint32_t)__popc(bal & lt)) & 1u;
     const uint32_t x = (incl << 1) ^ (0u - run) ^ X[b];  // x[b] = lo[b] ^ w[b]
+    X[b] = x;
     const uint32_t y = x ^ xp ^ cy;
     cy = maj3(x, xp, cy);
     const uint32_t v = y ^ y3 ^ cv;
@@ -179,23 +183,56 @@ struct LsShared {
   // (in bit 0), block + 1}, written with one 8-byte store so a reader that
   // sees the block number also sees the bit
   uint2 endw[kLsLanes][kLsWarps][2][32];
-  uint32_t final_lo[kLsLanes];
+  uint32_t hi_part[kLsLanes][kLsWarps];  // each warp's additive share of the final hi
+  uint32_t final_lo[kLsLanes], final_hi[kLsLanes];
 };
 
 // dynamic shared memory of one loscan CTA: the TMA stages, then LsShared
 constexpr uint32_t kLsSmem = kLsStageBytes * kLsStages + (uint32_t)sizeof(LsShared);
 
-// One CTA (kLsThreads threads): the lo chains of lanes lane0 .. lane0 +
-// kLsLanes - 1 of one entry over `rounds` rows of 1 KiB. map: the 4-D view
-// (box kLsLanes x 32 x 32 x kLsWarps), used when the entry has at least one
-// whole 1024-row segment. Writes the lo value that starts every ckrows-row
-// checkpoint segment to ck[seg * 256 + lane] and counts each checkpoint in
-// *progress (one increment per lane, release ordered); returns with the final
-// lo of lane lane0 + j in sh->final_lo[j] (after a block-wide barrier).
-// smem: kLsSmem bytes, 1024-byte aligned.
+// 435^e mod 2^32
+__device__ __forceinline__ uint32_t pow435u(uint64_t e) {
+  uint32_t r = 1u, b = 435u;
+  while (e) {
+    if (e & 1u) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+constexpr uint32_t kInv435 = 0xaff6957bu;  // 435^-1 mod 2^32
+constexpr uint32_t kHiOffset = 0xcbf29ce4u;  // hi half of the FNV-1a-64 offset basis
+
+// hi half of one segment's rows. X holds the x planes; turned back into row
+// words it gives x_r = lo_r ^ w_r of rows 32t + i, and
+//   hi' = 435 hi + c,  c = floor(435 x / 2^32) + (x << 8)  (mod 2^32)
+// is affine, so a segment adds sum_r 435^(rows after r) c_r to the chain's
+// final hi: Horner over the thread's 32 rows, scaled by 435^(32 (31 - t)),
+// summed over the warp. MASKED: only rows with their bit set in `valid`
+// count (a suffix of the segment is missing), `after` = valid rows after the
+// thread's last valid row.
+template <bool MASKED>
+__device__ __forceinline__ uint32_t ls_hi_segment(uint32_t (&X)[32], uint32_t scale, uint32_t valid) {
+  transpose32(X);
+  uint32_t a = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t x = X[i];
+    const uint32_t c = __umulhi(x, 435u) + (x << 8);
+    if (!MASKED || (valid >> i) & 1u) a = a * 435u + c;
+  }
+  return __reduce_add_sync(0xFFFFFFFFu, a * scale);
+}
+
+// One CTA (kLsThreads threads): the FNV-1a-64 chains of lanes lane0 ..
+// lane0 + kLsLanes - 1 of one entry over its `rounds` whole rows of 1 KiB --
+// the lo chain by the bitsliced scan, the hi chain from the x values the scan
+// leaves behind. map: the 4-D view (box kLsLanes x 32 x 32 x kLsWarps), used
+// when the entry has at least one whole 1024-row segment. Leaves lane
+// lane0 + j's state after the rounds in sh->final_lo[j], sh->final_hi[j]
+// (after a block-wide barrier). smem: kLsSmem bytes, 1024-byte aligned.
 __device__ __forceinline__ void loscan_cta(const CUtensorMap *map, const uint8_t *ptr, uint64_t rounds,
-                                           uint32_t lane0, uint32_t *ck, uint32_t ckrows, uint32_t *progress,
-                                           uint8_t *smem, LsShared *sh) {
+                                           uint32_t lane0, uint8_t *smem, LsShared *sh) {
   constexpr int M = kLsWarps;
   const int t = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t nfull = rounds >> 10;                   // whole 1024-row segments
@@ -230,6 +267,16 @@ __device__ __forceinline__ void loscan_cta(const CUtensorMap *map, const uint8_t
     const uint32_t lane = lane0 + l;
     // the warp whose end bits start this warp's segment
     const int pm = (m + M - 1) % M;
+    const uint32_t scale = pow435u(32u * (31u - (uint32_t)t));
+    // 435^(rows after the warp's current segment), stepped by 435^-(M * 1024)
+    uint32_t mul = (uint64_t)m < nfull ? pow435u(rounds - ((uint64_t)m + 1) * 1024u) : 0u;
+    const uint32_t step = [] {
+      uint32_t r = 1u, b = kInv435;
+      for (uint32_t e = M * 1024u; e; e >>= 1, b *= b)
+        if (e & 1u) r *= b;
+      return r;
+    }();
+    uint32_t hi = 0;
     for (uint64_t n = 0; n < nblk; ++n) {
       const int s = (int)(n % kLsStages);
       uint32_t X[32];
@@ -251,19 +298,14 @@ __device__ __forceinline__ void loscan_cta(const CUtensorMap *map, const uint8_t
       auto publish = [&](int b, uint32_t bit) {
         if (t == 0) st_volatile_shared2(&myend[b], bit, mytag);
       };
-      // segments past the last whole one (zero-filled by the TMA) leave the chain as it is
-      if (seg < nfull)
+      if (seg < nfull) {
         ls_planes<false>(X, 0u, start_bit, publish);
-      else
+        hi += mul * ls_hi_segment<false>(X, scale, 0u);
+      } else {
+        // past the last whole segment (zero-filled by the TMA): the chain stays as it is
         ls_planes<true>(X, 0u, start_bit, publish);
-      if (t == 0 && seg < nfull && (seg << 10) % ckrows == 0) {
-        // the segment's start value: every bit of the source's end word is published by now
-        ck[((seg << 10) / ckrows) * 256 + lane] = ls_gather(pend);
-        if (progress) {
-          __threadfence();
-          atomicAdd(progress, 1u);
-        }
       }
+      mul *= step;
     }
     // the last, partial segment (rows past the end masked): the warp that
     // follows the last whole segment runs it
@@ -283,17 +325,19 @@ __device__ __forceinline__ void loscan_cta(const CUtensorMap *map, const uint8_t
       ls_planes<true>(
           X, valid, [&](int b) -> uint32_t { return ls_await(&pend[b], stag); },
           [&](int b, uint32_t bit) { endw |= (bit & 1u) << b; });
-      if (t == 0 && tail0 % ckrows == 0) {
-        ck[(tail0 / ckrows) * 256 + lane] = ls_gather(pend);
-        if (progress) {
-          __threadfence();
-          atomicAdd(progress, 1u);
-        }
-      }
+      hi += ls_hi_segment<true>(X, pow435u(rounds > r + 32 ? rounds - (r + 32) : 0u), valid);
       if (t == 0) sh->final_lo[l] = endw;
     } else if (tail0 >= rounds && nfull > 0 && m == (int)((nfull - 1) % M)) {
       if (t == 0) sh->final_lo[l] = ls_gather(sh->endw[l][m][(nblk - 1) & 1]);
     }
+    if (t == 0) sh->hi_part[l][m] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x < kLsLanes) {
+    uint32_t hi = pow435u(rounds) * kHiOffset;
+#pragma unroll
+    for (int m = 0; m < M; ++m) hi += sh->hi_part[threadIdx.x][m];
+    sh->final_hi[threadIdx.x] = hi;
   }
   __syncthreads();
 }

@@ -228,6 +228,33 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                 hs = [None] * world
                 dist.all_gather_object(hs, _hash(buf))
                 check(f"large q={quant}: identical on all ranks", len(set(hs)) == 1)
+        if "config" in scenarios:
+            # BASELINE config sizes; inputs generated on the device from per-rank
+            # seeds, so any rank can regenerate a peer's chunk for the oracle
+            def gen(p, n, scale, seed):
+                gen_ = torch.Generator(device=dev).manual_seed(seed + p)
+                return torch.randn(n, generator=gen_, device=dev) * scale
+
+            big = DeviceRing(device=dev, capacity_bytes=2 << 30, timeout_s=60.0)
+            for tag, n, quant, scale in (("config2 plain AVG", 268_435_456, False, 1.0),
+                                         ("config3-chunk u8 AVG", 150_000_000 * world, True, 1e-2)):
+                seed = 4000 if not quant else 5000
+                buf = gen(big.position, n, scale, seed)
+                big.run_all_reduce(buf, "avg", quantize=quant)
+                torch.cuda.synchronize()
+                bounds = oring.chunk_bounds(n, world)
+                for c in sorted({big.position, (big.position + 1) % world}):
+                    lo, hi = bounds[c]
+                    spans = [gen((c + k) % world, n, scale, seed)[lo:hi].cpu().numpy() for k in range(world)]
+                    want = oring.reduce_chunk(spans, oring.ReduceOp.AVG, quant, world)
+                    check(f"{tag} chunk {c} ({hi - lo} elems)", buf[lo:hi].cpu().numpy().tobytes() == want.tobytes())
+                    del spans, want
+                hs = [None] * world
+                dist.all_gather_object(hs, _hash(buf))
+                check(f"{tag}: identical on all ranks", len(set(hs)) == 1)
+                del buf
+                torch.cuda.empty_cache()
+            big.close()
         ring.close()
         if rev is not None:
             rev.close()

@@ -93,20 +93,48 @@ def test_one_bit_drift_detected():
     assert simplehash(x) != h0
 
 
-@pytest.mark.parametrize("extra", [0, 1024 * 4096 - 1024, 3 * 1024 + 517, 1023, 1])
-def test_two_phase_big_entry_sizes(extra):
-    """Entries >= 64 MiB take the two-phase path (lo-chain checkpoints, segment
-    terms, combine): whole and partial last segments, tail words and bytes."""
+# sizes around the bitsliced kernel's block structure (5 warps x 1024-row
+# segments per block): whole / partial last block, partial last segment,
+# tail words and tail bytes
+BIG_SIZES = [64 << 20, (64 << 20) + 1023, (64 << 20) + 3 * 1024 + 517, (65 << 20), (65 << 20) + 1,
+             (66 << 20) + 4096 * 1024 - 1024, (67 << 20) + 7, (69 << 20) + 1024 * 1023 + 3]
+
+
+@pytest.mark.parametrize("n", BIG_SIZES)
+def test_big_entry_sizes(n):
+    """Entries >= 64 MiB take the bitsliced big-entry kernel (loscan.cuh: lo
+    chain by plane scans, hi chain affine): bit-exact against the oracle."""
     from paper_2505_14065_b200 import simplehash
 
-    n = (64 << 20) + extra
-    raw = np.random.default_rng(extra).integers(0, 256, n, dtype=np.uint8)
+    raw = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
     assert simplehash(to_dev(raw)) == osh.simplehash_c(raw)
 
 
-def test_two_phase_mixed_batch():
-    """Two big entries beside many small ones in one launch (config-4 shape):
-    phase-2 segment items interleave with ordinary items."""
+def test_big_entry_structured_words():
+    """All-zero, all-ones and alternating words: the carry planes of the
+    bitsliced multiply see long runs of identical bits."""
+    from paper_2505_14065_b200 import simplehash_many
+
+    n = (65 << 20) + 12
+    host = [np.zeros(n, np.uint8), np.full(n, 255, np.uint8),
+            np.tile(np.array([0xAA, 0x55, 0xFF, 0x00], np.uint8), n // 4)]
+    got = simplehash_many([to_dev(h) for h in host])
+    assert got == osh.simplehash_many_c(host, threads=3)
+
+
+def test_big_entry_unaligned_base_uses_batch_path():
+    """A >= 64 MiB view at a byte offset (not 16-byte aligned, no TMA view):
+    hashed by the batch kernel's direct loads, same digest as the oracle."""
+    from paper_2505_14065_b200 import simplehash
+
+    raw = np.random.default_rng(3).integers(0, 256, (64 << 20) + 9, dtype=np.uint8)
+    dev = to_dev(raw)
+    assert simplehash(dev[1:]) == osh.simplehash_c(raw[1:])
+
+
+def test_big_entries_mixed_batch():
+    """Two big entries beside many small ones in one call (config-4 shape):
+    the big-entry kernel runs concurrently with the batch kernel."""
     from paper_2505_14065_b200 import simplehash_many
 
     rng = np.random.default_rng(77)
@@ -116,7 +144,7 @@ def test_two_phase_mixed_batch():
     assert got == osh.simplehash_many_c(host, threads=8)
 
 
-def test_two_phase_repeated_calls_stable():
+def test_big_entries_repeated_calls_stable():
     from paper_2505_14065_b200 import simplehash_many
 
     x = torch.randint(0, 256, (200 << 20,), dtype=torch.uint8, device="cuda")

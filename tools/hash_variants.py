@@ -1,8 +1,9 @@
 """Microbenchmark of the simplehash kernel variants (PCCLB_HASH_VARIANT).
 
 Run one variant per process:  PCCLB_HASH_VARIANT=k python tools/hash_variants.py
-Prints one JSON line: config-4 layout, a single 1.05 GB entry, and 64 equal
-64 MiB entries (HBM-bound case), each as ms and GB/s (CUDA events)."""
+Prints one JSON line: config-4 layout (whole, its two 1.05 GB entries alone,
+the other 289 alone), a single 1.05 GB entry, and 64 equal 64 MiB entries
+(HBM-bound case), each as ms and GB/s (CUDA events)."""
 
 import json
 import os
@@ -49,6 +50,9 @@ for _, n in layout:
     off += n
 res = {"variant": int(os.environ.get("PCCLB_HASH_VARIANT", "0"))}
 res["config4"], digests = timeit(views, 7)
+# the two largest entries (the bitsliced kernel's share) and the rest alone
+res["config4_big2"], _ = timeit([views[0], views[-1]], 5)
+res["config4_rest"], _ = timeit(views[1:-1], 5)
 res["single_1GB"], _ = timeit([views[0]], 5)
 eq = state[: 64 * (32 << 20)].view(64, -1)
 res["64x64MiB"], _ = timeit([eq[i] for i in range(64)], 7)

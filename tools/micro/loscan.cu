@@ -12,13 +12,13 @@
 #include "../../paper_2505_14065_b200/csrc/loscan.cuh"
 
 __global__ void __launch_bounds__(pcclb::kLsThreads, 1)
-    loscan_kernel(const __grid_constant__ CUtensorMap map, const uint8_t *ptr, uint64_t rounds, uint32_t *ck,
-                  uint32_t *lofinal, uint32_t *progress) {
+    loscan_kernel(const __grid_constant__ CUtensorMap map, const uint8_t *ptr, uint64_t rounds, uint64_t *fin) {
   extern __shared__ __align__(1024) uint8_t smem[];
   auto *sh = reinterpret_cast<pcclb::LsShared *>(smem + pcclb::kLsStageBytes * pcclb::kLsStages);
   const uint32_t lane0 = blockIdx.x * pcclb::kLsLanes;
-  pcclb::loscan_cta(&map, ptr, rounds, lane0, ck, 32768u, progress + blockIdx.x, smem, sh);
-  if (threadIdx.x < pcclb::kLsLanes) lofinal[lane0 + threadIdx.x] = sh->final_lo[threadIdx.x];
+  pcclb::loscan_cta(&map, ptr, rounds, lane0, smem, sh);
+  if (threadIdx.x < pcclb::kLsLanes)
+    fin[lane0 + threadIdx.x] = ((uint64_t)sh->final_hi[threadIdx.x] << 32) | sh->final_lo[threadIdx.x];
 }
 
 static bool encode4d(CUtensorMap *m, const void *p, uint64_t rounds) {
@@ -54,15 +54,12 @@ __global__ void fill(uint32_t *p, uint64_t n, uint32_t seed) {
   }
 }
 
-// serial reference: one thread per lane
-__global__ void serial_lo(const uint32_t *p, uint64_t rounds, uint32_t *ck, uint32_t *fin, uint32_t ckrows) {
+// serial reference: one thread per lane, the full FNV-1a-64 chain
+__global__ void serial_fnv(const uint32_t *p, uint64_t rounds, uint64_t *fin) {
   const uint32_t lane = threadIdx.x + blockIdx.x * blockDim.x;
-  uint32_t lo = 0x84222325u;
-  for (uint64_t r = 0; r < rounds; ++r) {
-    if (r % ckrows == 0) ck[(r / ckrows) * 256 + lane] = lo;
-    lo = (lo ^ p[r * 256 + lane]) * 435u;
-  }
-  fin[lane] = lo;
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint64_t r = 0; r < rounds; ++r) h = (h ^ p[r * 256 + lane]) * 0x100000001b3ull;
+  fin[lane] = h;
 }
 
 int main(int argc, char **argv) {
@@ -70,22 +67,18 @@ int main(int argc, char **argv) {
   const uint64_t extra = argc > 2 ? strtoull(argv[2], 0, 10) : 0;  // extra rows past whole MiB
   const uint64_t rounds = mib * 1024 + extra;
   const uint64_t words = rounds * 256;
-  const uint32_t ckrows = 32768;
-  const uint64_t nseg = (rounds + ckrows - 1) / ckrows;
-  uint32_t *d, *ck0, *ck1, *fin0, *fin1, *prog;
-  CK(cudaMalloc(&d, words * 4));
-  CK(cudaMalloc(&ck0, nseg * 256 * 4));
-  CK(cudaMalloc(&ck1, nseg * 256 * 4));
-  CK(cudaMalloc(&fin0, 256 * 4));
-  CK(cudaMalloc(&fin1, 256 * 4));
-  CK(cudaMalloc(&prog, 4096));
+  uint32_t *d;
+  uint64_t *fin0, *fin1;
+  CK(cudaMalloc(&d, words * 4 + 4));
+  CK(cudaMalloc(&fin0, 256 * 8));
+  CK(cudaMalloc(&fin1, 256 * 8));
   fill<<<1184, 512>>>(d, words, 12345u);
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  serial_lo<<<8, 32>>>(d, rounds, ck0, fin0, ckrows);
+  serial_fnv<<<8, 32>>>(d, rounds, fin0);
   cudaEventRecord(b);
   CK(cudaEventSynchronize(b));
   float ms0;
@@ -95,11 +88,10 @@ int main(int argc, char **argv) {
   CK(cudaFuncSetAttribute(loscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pcclb::kLsSmem));
   float best = 1e9;
   for (int it = 0; it < 5; ++it) {
-    CK(cudaMemset(ck1, 0xff, nseg * 256 * 4));
-    CK(cudaMemset(prog, 0, 4096));
+    CK(cudaMemset(fin1, 0xff, 256 * 8));
     cudaEventRecord(a);
     loscan_kernel<<<256 / pcclb::kLsLanes, pcclb::kLsThreads, pcclb::kLsSmem>>>(
-        map, reinterpret_cast<const uint8_t *>(d), rounds, ck1, fin1, prog);
+        map, reinterpret_cast<const uint8_t *>(d), rounds, fin1);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     CK(cudaGetLastError());
@@ -107,13 +99,10 @@ int main(int argc, char **argv) {
     cudaEventElapsedTime(&ms, a, b);
     if (ms < best) best = ms;
   }
-  std::vector<uint32_t> h0(nseg * 256), h1(nseg * 256), f0(256), f1(256);
-  CK(cudaMemcpy(h0.data(), ck0, nseg * 1024, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(h1.data(), ck1, nseg * 1024, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(f0.data(), fin0, 1024, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(f1.data(), fin1, 1024, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> f0(256), f1(256);
+  CK(cudaMemcpy(f0.data(), fin0, 2048, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(f1.data(), fin1, 2048, cudaMemcpyDeviceToHost));
   uint64_t bad = 0;
-  for (uint64_t i = 0; i < nseg * 256; ++i) bad += h0[i] != h1[i];
   for (int i = 0; i < 256; ++i) bad += f0[i] != f1[i];
   printf("rows=%llu serial %.3f ms  bitsliced %.3f ms (%.1f GB/s)  mismatches=%llu\n",
          (unsigned long long)rounds, ms0, best, words * 4 / best / 1e6, (unsigned long long)bad);
