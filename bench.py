@@ -221,16 +221,40 @@ def bench_hash(args, rank, world, local):
     clk = clocks.stop()
     barrier(world)
     ms_max = max_over_ranks(ms, world)
-    launches = args.steps  # one multi-entry launch per step
+    launches = 2 * args.steps  # per step: the batch kernel + the big-entry kernel
 
-    # single largest entry alone: chain-latency bound reference point
-    big = views[0]
-    t0.record(stream)
-    for _ in range(3):
-        simplehash_many_async([big], out[:1])
-    t1.record(stream)
-    torch.cuda.synchronize(dev)
-    big_ms = t0.elapsed_time(t1) / 3
+    # the two 1.05 GB entries alone (the bitsliced big-entry kernel) and the
+    # other 289 alone (the TMA batch kernel): how the concurrent launch overlaps
+    def time_views(vs, reps=3):
+        simplehash_many_async(vs, out[: len(vs)])
+        t0.record(stream)
+        for _ in range(reps):
+            simplehash_many_async(vs, out[: len(vs)])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        return t0.elapsed_time(t1) / reps
+
+    big_ms = time_views([views[0], views[-1]])
+    rest_ms = time_views(views[1:-1])
+
+    # parity outside the timed region: every digest against the C oracle
+    parity = None
+    if not args.no_parity:
+        from oracle import simplehash as osh
+
+        simplehash_many_async(views, out)
+        got = [int(x) & 0xFFFFFFFFFFFFFFFF for x in out.cpu().tolist()]
+        host = state.view(torch.uint8).cpu().numpy()
+        bufs, off = [], 0
+        for _, n in layout:
+            bufs.append(host[off : off + 2 * n])
+            off += 2 * n
+        order = sorted(range(len(bufs)), key=lambda i: -bufs[i].size)
+        want = dict(zip(order, osh.simplehash_many_c([bufs[i] for i in order], threads=os.cpu_count() or 8)))
+        bad = sum(got[i] != want[i] for i in range(len(bufs)))
+        parity = {"status": "ok" if bad == 0 else "MISMATCH", "checked": f"{len(bufs) - bad}/{len(bufs)} digests "
+                  "equal oracle/simplehash.c (all 291 entries, 16.06 GB)"}
+        del host, bufs
 
     # e2e: host state (pinned) -> device, hash, digests -> host
     e2e = None
@@ -258,8 +282,6 @@ def bench_hash(args, rank, world, local):
 
     pk = peaks()
     achieved = nbytes / (ms * 1e-3) / 1e9
-    sm_mhz = (clk or {}).get("sm_mhz") or 1965
-    chain_floor_ms = (views[0].numel() * 2 // 1024) * 10.5 / (sm_mhz * 1e6) * 1e3
     result = {
         "value": round(world * nbytes / (ms_max * 1e-3) / 1e9, 2),
         "unit": "GB/s",
@@ -273,14 +295,13 @@ def bench_hash(args, rank, world, local):
                      "frac": round(achieved / pk["hbm_gbs"], 4),
                      "traffic": ncu_traffic("hash_config4"),
                      "peak_src": pk["src"],
-                     "kernel": "simplehash_batch_kernel", "algorithmic_bytes_per_launch": nbytes,
-                     "largest_entry_alone_ms": round(big_ms, 3),
-                     "largest_entry_alone_gbs": round(views[0].numel() * 2 / (big_ms * 1e-3) / 1e9, 1),
-                     # the largest entry's 256 lanes are serial chains: even the lo-chain
-                     # phase needs 10.5 cycles per 1 KiB row (tools/micro/chain_lds.cu)
-                     "latency_floor_ms": round(chain_floor_ms, 3),
-                     "frac_of_latency_floor": round(chain_floor_ms / ms, 4),
+                     "kernel": "simplehash_batch_kernel (289 entries, TMA ring) + simplehash_big_kernel "
+                               "(the two 1.05 GB entries, bitsliced lo scan), one call, concurrent",
+                     "algorithmic_bytes_per_launch": nbytes,
+                     "big_entries_alone_ms": round(big_ms, 3),
+                     "rest_alone_ms": round(rest_ms, 3),
                      "hbm_floor_ms": round(nbytes / (pk["hbm_gbs"] * 1e9) * 1e3, 3)},
+        "parity": parity,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -378,6 +399,35 @@ def bench_allreduce(args, rank, world, local, quantize=False):
         e2e_alg = S / (e2e_ms * 1e-3) / 1e9
         e2e = {"value": round(e2e_alg * 2 * (world - 1) / world if world > 1 else e2e_alg, 2), "unit": "GB/s",
                "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "ms_per_step": round(e2e_ms, 3)}
+    # parity outside the timed region: one fresh all-reduce of the seeded
+    # inputs; every rank checks the chunk it owns against the oracle (peers'
+    # inputs regenerated from their seeds on this device)
+    parity = None
+    if not args.no_parity:
+        from oracle import ring as oring
+
+        buf.copy_(src)
+        ring.run_all_reduce(buf, op, quantize=quantize)
+        torch.cuda.synchronize(dev)
+        scale = 1e-2 if quantize else 1.0
+
+        def peer_input(p):
+            gp = torch.Generator(device=dev).manual_seed(p)
+            return torch.randn(n, generator=gp, device=dev) * scale
+
+        bounds = oring.chunk_bounds(n, world)
+        c = (ring.position + 1) % world  # the chunk this position owns (folded last here)
+        lo, hi = bounds[c]
+        spans = [peer_input((c + k) % world)[lo:hi].cpu().numpy() for k in range(world)]
+        if world > 1:
+            want = oring.reduce_chunk(spans, oring.ReduceOp.AVG, quantize, world)
+        else:  # W = 1: finalize only, never quantized (client.py:896-900)
+            want = spans[0]
+        ok = buf[lo:hi].cpu().numpy().tobytes() == want.tobytes()
+        ok = max_over_ranks(0.0 if ok else 1.0, world) == 0.0
+        parity = {"status": "ok" if ok else "MISMATCH",
+                  "checked": f"the chunk each of the {world} ranks owns ({hi - lo} elements) "
+                             "bit-equal to oracle.ring.reduce_chunk"}
     nvl_bytes = 2 * (world - 1) / world * S  # per-GPU NVLink ingress (plain)
     # plain: fold, push gather, 3 barriers; quantized (fused schedule): range,
     # barrier 0, W-1 step kernels, the fused adoption+gather kernel
@@ -420,6 +470,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
                    "buffer": "unregistered (staged copy-in)" if args.no_register else "registered once (DeviceRing.register, zero-copy reads)",
                    "busbw_definition": "algbw*2(W-1)/W", "l2": "1 GiB inputs > 126 MB L2"},
         "roofline": roof,
+        "parity": parity,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches_per_op * args.steps,
@@ -593,6 +644,7 @@ def main():
     ap.add_argument("--elems", type=int, default=0, help="override elements per GPU (allreduce/quant/local)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check after the timed region")
     ap.add_argument("--no-register", action="store_true", help="all-reduce: stage through the workspace instead of registering the buffer")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
