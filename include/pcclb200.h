@@ -180,8 +180,10 @@ PCCLB_API int pcclb_ring_export(pcclb_ring *r, void *handle64_out);
 /* Map peer `peer`'s workspace (handle from its pcclb_ring_export). */
 PCCLB_API int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle64);
 /* Host-mapped abort word the control plane may set (reference: the tag box
- * abort_event set on ABORT_NOTIFY, client.py:196-204). Returns host pointer. */
-PCCLB_API volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r);
+ * abort_event set on ABORT_NOTIFY, client.py:196-204). Returns host pointer.
+ * Attempt-scoped: storing A aborts every attempt <= A at its next barrier,
+ * vote or fused-step poll; later attempts are unaffected (no reset needed). */
+PCCLB_API volatile uint64_t *pcclb_ring_abort_word(pcclb_ring *r);
 /* Number of engines that may run ops concurrently on this GPU (the
  * communicator's pool of slots, client.py:482-486; default 2). The fused
  * quantized steps spin on peer-ready flags with persistent CTAs, so each engine

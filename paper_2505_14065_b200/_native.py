@@ -96,7 +96,7 @@ SIGNATURES = {
     "pcclb_ring_create": (_I, [_I, _U32, _U32, _U64, ctypes.POINTER(_P)]),
     "pcclb_ring_export": (_I, [_P, _P]),
     "pcclb_ring_import": (_I, [_P, _U32, _P]),
-    "pcclb_ring_abort_word": (ctypes.POINTER(ctypes.c_uint32), [_P]),
+    "pcclb_ring_abort_word": (ctypes.POINTER(ctypes.c_uint64), [_P]),
     "pcclb_ring_capacity": (_U64, [_P, _I, _I]),
     "pcclb_ring_set_slots": (_I, [_P, _U32]),
     "pcclb_ring_workspace_bytes": (_U64, [_U64, _U32, _I, _I]),

@@ -174,7 +174,6 @@ class Communicator:
         # the slot stream sees the caller's writes to the buffer
         stream.wait_stream(torch.cuda.current_stream(self.device))
         engine = self.engines[slot]
-        engine.reset_abort()
         self.stats["reduce_attempts"] += 1
         try:
             ticket = engine.all_reduce_async(buffer, op, quantize=quantize, stream=stream)
@@ -207,9 +206,13 @@ class Communicator:
         return self.await_async_reduce(self.all_reduce_async(buffer, tag, op, quantize))
 
     def abort(self, tag: int) -> None:
-        """ABORT_NOTIFY for `tag` (client.py:196-204): the slot's in-flight
-        attempt aborts at its next barrier and restores the buffer."""
-        self.engines[tag % self.pool_size].signal_abort()
+        """ABORT_NOTIFY for `tag` (client.py:196-204): the tag's in-flight
+        attempt aborts at its next barrier (or its completion vote) on every
+        rank and restores the buffer; ops of other tags queued on the same
+        slot are not affected (the abort word is attempt-scoped)."""
+        h = self._handles.get(tag)
+        if h is not None and h.pending and h.ticket is not None:
+            self.engines[h.slot].signal_abort(h.ticket.attempt)
 
     def restore(self, handle: AsyncHandle, buffer: torch.Tensor) -> None:
         """Completion vetoed (client.py:973-983): hand back the input bytes."""

@@ -96,12 +96,16 @@ struct Signal {
   pcclb_qmeta qmeta[kIpcMaxWorld];      // written by the predecessor: meta of its step-s codes
   uint32_t claim[kIpcMaxWorld + 1];     // fused quantized steps + gather: work counters
   pcclb_qmeta gmeta[kIpcMaxWorld];      // written by chunk c's owner: meta of its final codes
+  uint64_t vote[kIpcMaxWorld];          // coordinator only: peer j's completion vote (attempt << 8 | failed)
+  uint64_t decision;                    // written by the coordinator: attempt << 8 | 1 commit / 2 abort
 };
 static_assert(sizeof(Signal) <= kSignalBytes, "signal area too small");
 
 struct HostFlags {
-  volatile uint32_t abort;  // set by the control plane
-  uint32_t pad[15];
+  // set by the control plane: every attempt <= abort aborts (attempt-scoped,
+  // so queued later attempts are not affected and nothing needs resetting)
+  volatile uint64_t abort;
+  uint64_t pad[7];
 };
 
 __device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__
     uint32_t v = *(volatile uint32_t *)&me->status;
     if (v == 0) {
       if (a.fault) v = PCCLB_EIO;
-      else if (a.host->abort) v = PCCLB_EABORTED;
+      else if (a.host->abort >= a.attempt) v = PCCLB_EABORTED;
       else if (a.check_range && a.check_range->nonfinite) v = PCCLB_ENONFINITE;
     }
     s_verdict = v;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(64) ipc_barrier_kernel(const __grid_constant__
           if (j != a.rank && *(volatile uint64_t *)&me->desc[j] != a.desc) verdict = PCCLB_EINVAL;
       break;
     }
-    if (a.host->abort) {
+    if (a.host->abort >= a.attempt) {
       verdict = PCCLB_EABORTED;
       break;
     }
@@ -208,6 +212,93 @@ __device__ __forceinline__ uint64_t dpeel16(const void *p) {
 
 __device__ __forceinline__ bool op_failed(const Signal *me) {
   return *(volatile const uint32_t *)&me->status != 0;
+}
+
+// ---------------------------------------------------------------------------
+// completion vote (reference COLLECTIVE_COMPLETE_VOTE, client.py:950-983):
+// the op commits on every rank or on none
+// ---------------------------------------------------------------------------
+// Every rank posts its outcome to the coordinator (ring position 0) after all
+// of its kernels of the attempt -- including remote stores into peers'
+// buffers, so a vote also means "my pushes into you landed"; the coordinator
+// waits for every vote and posts one decision to every rank; a rank adopts
+// it. Any failure (own, a peer's, a missing vote, the host abort word)
+// decides "abort" everywhere and the restore kernel that follows puts the
+// caller's bytes back on every rank. Without a coordinator decision (the
+// coordinator died), the wait times out and the rank aborts.
+struct VoteArgs {
+  Signal *mine;
+  Signal *peer[kIpcMaxWorld];
+  const HostFlags *host;
+  uint64_t attempt;
+  uint64_t timeout_ns;
+  uint32_t rank, world, coord;
+  uint32_t fault;  // 1: inject a local failure at the vote
+};
+
+__global__ void __launch_bounds__(32) ipc_vote_kernel(const __grid_constant__ VoteArgs a) {
+  if (threadIdx.x != 0) return;
+  Signal *me = a.mine;
+  uint32_t st = *(volatile uint32_t *)&me->status;
+  if (st == 0 && a.fault) st = PCCLB_EIO;
+  if (st == 0 && a.host->abort >= a.attempt) st = PCCLB_EABORTED;
+  const uint64_t tag = a.attempt << 8;
+  __threadfence_system();  // this rank's earlier remote stores before its vote
+  st_release_sys(&a.peer[a.coord]->vote[a.rank], tag | (st ? 1u : 0u));
+  uint64_t decision = 0;
+  const uint64_t t0 = globaltimer();
+  if (a.rank == a.coord) {
+    bool commit = st == 0;
+    for (uint32_t j = 0; j < a.world; ++j) {
+      if (j == a.rank) continue;
+      uint64_t v;
+      while (((v = ld_acquire_sys(&me->vote[j])) >> 8) != a.attempt) {
+        if (globaltimer() - t0 > a.timeout_ns) break;
+        __nanosleep(32);
+      }
+      if ((v >> 8) != a.attempt || (v & 0xff) != 0) commit = false;
+    }
+    decision = tag | (commit ? 1u : 2u);
+    for (uint32_t j = 0; j < a.world; ++j)
+      if (j != a.rank) st_release_sys(&a.peer[j]->decision, decision);
+  } else {
+    while (((decision = ld_acquire_sys(&me->decision)) >> 8) != a.attempt) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        decision = tag | 2u;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  if ((decision & 0xff) != 1u && st == 0) st = PCCLB_EABORTED;  // vetoed by a peer's failure
+  *(volatile uint32_t *)&me->status = st;
+}
+
+// puts the caller's bytes back (collective.py:568-574) when the attempt
+// failed -- on the device, in stream order, so a later op queued on the same
+// engine copies in (and overwrites the backup) only after the restore
+__global__ void __launch_bounds__(kIpcThreads) ipc_restore_kernel(const Signal *me, const uint8_t *bak, uint8_t *buf,
+                                                                   uint64_t nbytes) {
+  if (!op_failed(me)) return;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  // 16-byte vectors when bak and buf share their offset modulo 16, else
+  // words (f32/f64 buffers are 4-byte aligned; the backup starts 16-aligned)
+  const uintptr_t pb = reinterpret_cast<uintptr_t>(buf), pk = reinterpret_cast<uintptr_t>(bak);
+  const uint32_t g = ((pb ^ pk) & 15) == 0 ? 16u : ((pb ^ pk) & 3) == 0 ? 4u : 1u;
+  uint64_t head = (g - (pb & (g - 1))) & (g - 1);
+  if (head > nbytes) head = nbytes;
+  const uint64_t nv = (nbytes - head) / g;
+  if (g == 16)
+    for (uint64_t v = tid; v < nv; v += nth)
+      reinterpret_cast<uint4 *>(buf + head)[v] = reinterpret_cast<const uint4 *>(bak + head)[v];
+  else if (g == 4)
+    for (uint64_t v = tid; v < nv; v += nth)
+      reinterpret_cast<uint32_t *>(buf + head)[v] = reinterpret_cast<const uint32_t *>(bak + head)[v];
+  else
+    for (uint64_t v = tid; v < nv; v += nth) buf[head + v] = bak[head + v];
+  for (uint64_t i = tid; i < head; i += nth) buf[i] = bak[i];
+  for (uint64_t i = head + nv * g + tid; i < nbytes; i += nth) buf[i] = bak[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -694,7 +785,7 @@ __device__ uint32_t qwait(const A &a, const uint64_t *flag) {
       const uint32_t st = *(volatile uint32_t *)&a.mine->status;
       if (st) return st;
       if ((it & 7) == 0) {
-        if (a.host->abort) return PCCLB_EABORTED;
+        if (a.host->abort >= a.attempt) return PCCLB_EABORTED;
         for (uint32_t j = 0; j < a.world; ++j)
           if (j != a.rank && ld_relaxed_sys(&a.mine->abort_tok[j]) == a.attempt) return PCCLB_EABORTED;
         if (globaltimer() - t0 > a.timeout_ns) return PCCLB_ETIMEOUT;
@@ -906,7 +997,7 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(cons
   const uint64_t npos = rounds * w;
   if (threadIdx.x == 0 && *(volatile uint32_t *)&a.mine->status == 0) {
     if (blockIdx.x == 0 && a.fault) qfail(a, PCCLB_EIO);
-    else if (a.host->abort) qfail(a, PCCLB_EABORTED);
+    else if (a.host->abort >= a.attempt) qfail(a, PCCLB_EABORTED);
     else if (on && a.orange->nonfinite) qfail(a, PCCLB_ENONFINITE);
   }
   const QParams qp = qparams_from_range(*a.orange);
@@ -1109,6 +1200,30 @@ unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
   return grid_for(n_vec, kIpcThreads, ctas_per_sm);
 }
 
+// The attempt's last two kernels: completion vote (fault point `index`),
+// then the device-side restore of a failed attempt.
+int launch_vote_and_restore(pcclb_ring *r, void *buf, uint64_t nbytes, uint64_t attempt, uint32_t index,
+                            int fault_at, uint64_t timeout_ns, cudaStream_t s) {
+  VoteArgs a{};
+  a.mine = sig_of(r->ws);
+  for (uint32_t j = 0; j < r->world; ++j) a.peer[j] = sig_of(r->peer_ws[j]);
+  a.host = r->host_dev;
+  a.attempt = attempt;
+  a.timeout_ns = timeout_ns;
+  a.rank = r->rank;
+  a.world = r->world;
+  a.coord = 0;
+  a.fault = (fault_at >= 0 && (uint32_t)fault_at == index) ? 1u : 0u;
+  ipc_vote_kernel<<<1, 32, 0, s>>>(a);
+  PCCLB_LAUNCH_CHECK();
+  if (nbytes) {
+    ipc_restore_kernel<<<ipc_grid(nbytes / 16 + 1, 2), kIpcThreads, 0, s>>>(
+        a.mine, reinterpret_cast<const uint8_t *>(r->ws + kSignalBytes), static_cast<uint8_t *>(buf), nbytes);
+    PCCLB_LAUNCH_CHECK();
+  }
+  return PCCLB_OK;
+}
+
 // dequant-accumulate shape (experiments): PCCLB_DQA=0 16 floats x 2 (default),
 // 1: 4 floats x 4, 2: 16 floats x 4
 int dqa_mode_value() {
@@ -1303,8 +1418,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
       ipc_push_kernel<T><<<ipc_grid(own_n / Pack16<T>::N + 1, 2), kIpcThreads, 0, s>>>(pa);
       PCCLB_LAUNCH_CHECK();
     }
-    rc = launch_barrier(r, attempt, 2, fault_at, nullptr, timeout_ns, s);
-    if (rc) return rc;
+    // the vote that follows also tells every rank that all pushes into it landed
   } else if (jobs && (gather_on_copy_engines() || gather_mode() == 2)) {
     // verbatim chunk copies on the copy engines (759 GB/s per direction for
     // plain peer allocations in tools/micro/p2p_micro.cu). CE copies cannot
@@ -1335,6 +1449,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     }
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
+  rc = launch_vote_and_restore(r, buf, n * sizeof(T), attempt, 2, fault_at, timeout_ns, s);
+  if (rc) return rc;
   r->timer.mark(s);
   return PCCLB_OK;
 }
@@ -1533,6 +1650,9 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     ipc_qfinal_kernel<<<grid, kQThreads, 0, s>>>(g);
     PCCLB_LAUNCH_CHECK();
     r->timer.mark(s);
+    rc = launch_vote_and_restore(r, buf, n * sizeof(float), attempt, w, fault_at, timeout_ns, s);
+    if (rc) return rc;
+    r->timer.mark(s);
     return PCCLB_OK;
   }
   // gather prologue: owner adopts D(Q(own)) (collective.py:538-551), fused with AVG
@@ -1576,6 +1696,9 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     ipc_gather_quant_kernel<<<ipc_grid(maxn / 4 + 1, occ < 1 ? 1 : occ), kIpcThreads, 0, s>>>(g, jobs, vec);
     PCCLB_LAUNCH_CHECK();
   }
+  r->timer.mark(s);
+  rc = launch_vote_and_restore(r, buf, n * sizeof(float), attempt, w, fault_at, timeout_ns, s);
+  if (rc) return rc;
   r->timer.mark(s);
   return PCCLB_OK;
 }
@@ -1662,7 +1785,7 @@ int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots) {
   return PCCLB_OK;
 }
 
-volatile uint32_t *pcclb_ring_abort_word(pcclb_ring *r) { return r ? &r->host->abort : nullptr; }
+volatile uint64_t *pcclb_ring_abort_word(pcclb_ring *r) { return r ? &r->host->abort : nullptr; }
 
 uint64_t pcclb_ring_capacity(pcclb_ring *r, int dtype, int quantize) {
   if (!r || !valid_dtype(dtype)) return 0;
@@ -1767,10 +1890,7 @@ int pcclb_ring_wait(pcclb_ring *r, uint32_t ticket, pcclb_stats *out_stats) {
   // `in` holds the op's input in both modes (copy-in, or the backup CTAs of
   // a zero-copy fold, which run even when the op failed)
   r->have_backup = w > 1;
-  if (st == 0) return PCCLB_OK;
-  // restore the caller's bytes (collective.py:568-574)
-  PCCLB_CUDA(cudaMemcpyAsync(o.buf, r->ws + kSignalBytes, o.n * esz, cudaMemcpyDeviceToDevice, o.stream));
-  PCCLB_CUDA(cudaStreamSynchronize(o.stream));
+  // a failed attempt was restored on the device, in stream order (ipc_restore_kernel)
   return (int)st;
 }
 

@@ -42,10 +42,11 @@ class ReduceStats:
 class RingTicket:
     """An enqueued all-reduce attempt (the AsyncHandle of client.py:102-127)."""
 
-    def __init__(self, ring: "DeviceRing", index: int, buffer: torch.Tensor):
+    def __init__(self, ring: "DeviceRing", index: int, buffer: torch.Tensor, attempt: int = 0):
         self.ring = ring
         self.index = index
         self.buffer = buffer  # kept alive while the engine owns it
+        self.attempt = attempt
         self.consumed = False
 
 
@@ -81,6 +82,7 @@ class DeviceRing:
         self._handle = None
         self._capacity = 0
         self._registered: dict[int, torch.Tensor] = {}  # slot -> tensor (kept alive)
+        self._pending = 0  # enqueued attempts not yet awaited
         # engines sharing this GPU concurrently (the communicator's pool size)
         self.slots = max(1, int(slots))
         self._create(capacity_bytes)
@@ -133,9 +135,22 @@ class DeviceRing:
         return need + 4096
 
     def ensure_capacity(self, n: int, dtype: torch.dtype, quantize: bool) -> None:
+        """Grow the workspace for an n-element op. Growing is collective (every
+        rank re-exports its workspace), so it is refused while attempts are in
+        flight, and the ranks first agree on (n, dtype, quantize): SPMD callers
+        all reach this point together; ranks that disagree all raise
+        UsageError. (A rank whose op still fits does not take part -- with
+        mismatched sizes that rank's attempt then fails at its first barrier.)"""
         code = DTYPE_CODE[dtype]
         if lib().pcclb_ring_capacity(self._handle, code, int(quantize)) >= n:
             return
+        if self._pending:
+            raise UsageError("workspace must grow, but attempts are in flight: await them first")
+        key = (int(n), int(code), bool(quantize))
+        keys: list = [None] * self.world
+        dist.all_gather_object(keys, key, group=self.group)
+        if any(k != key for k in keys):
+            raise UsageError(f"ranks disagree on the op that grows the workspace: {sorted(set(keys))}")
         esz = torch.tensor([], dtype=dtype).element_size()
         self._create(self.required_bytes(n, self.world, esz, quantize))
 
@@ -171,13 +186,19 @@ class DeviceRing:
             del self._registered[slot]
 
     # -- control-plane hooks --
-    def signal_abort(self) -> None:
-        """Raise the host abort word (the tag box abort_event, client.py:196-204)."""
-        self._abort[0] = 1
+    def signal_abort(self, attempt: int | None = None) -> None:
+        """Abort attempts up to `attempt` (the tag box abort_event set on
+        ABORT_NOTIFY, client.py:196-204). The word is attempt-scoped: it
+        aborts every attempt <= the value at its next barrier, vote or poll,
+        and no later one. Default: the attempt in flight and the next one
+        enqueued (an abort raised just before the op)."""
+        a = self._attempt + 1 if attempt is None else int(attempt)
+        if a > self._abort[0]:
+            self._abort[0] = a
 
     def reset_abort(self) -> None:
-        """Clear the abort word for a new attempt (box.reset_for_attempt)."""
-        self._abort[0] = 0
+        """Kept for the reference's box.reset_for_attempt call sites: an
+        attempt-scoped abort word never needs clearing."""
 
     # -- the op --
     def _validate(self, buffer: torch.Tensor, op, quantize: bool):
@@ -207,7 +228,8 @@ class DeviceRing:
             self._attempt, fault_at, self.timeout_s, s, ctypes.byref(t),
         )
         self._raise_for(rc, "ring_enqueue")
-        return RingTicket(self, int(t.value), buffer)
+        self._pending += 1
+        return RingTicket(self, int(t.value), buffer, self._attempt)
 
     def _raise_for(self, rc: int, what: str) -> None:
         if rc == _native.PCCLB_OK:
@@ -222,10 +244,14 @@ class DeviceRing:
 
     def await_reduce(self, ticket: "RingTicket") -> ReduceStats:
         """Block until the attempt resolves; raises CollectiveAborted after the
-        buffer was restored (collective.py:568-574)."""
+        buffer was restored (collective.py:568-574). Every rank reaches the
+        same outcome: the attempt ends with a completion vote on the device
+        (the reference's COLLECTIVE_COMPLETE_VOTE), and a failure anywhere
+        restores the buffers of all ranks."""
         if ticket.consumed:
             raise UsageError("ticket already awaited")
         ticket.consumed = True
+        self._pending -= 1
         stats = Stats()
         rc = lib().pcclb_ring_wait(self._handle, ticket.index, ctypes.byref(stats))
         self._raise_for(rc, "ring_wait")

@@ -72,7 +72,8 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
         if "faults" in scenarios:
             n = 40_003
             for quant in (False, True):
-                nb = world if quant else 2
+                # every abort point: the barriers / fused steps and the completion vote
+                nb = world + 1 if quant else 3
                 for k in range(nb):
                     f = k % world
                     inputs = ring_inputs(world, n, np.dtype("float32"), 500 + k)
@@ -107,6 +108,26 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             ring.run_all_reduce(buf, "avg")
             want = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.AVG)
             check("host abort: retry exact", buf.cpu().numpy().tobytes() == want.tobytes())
+            # abort raised while the attempt runs (after enqueue): the completion vote
+            # makes every rank end the same way -- all aborted with their bytes back,
+            # or all completed bit-exact
+            for qi, quant in enumerate((False, True)):
+                inputs = ring_inputs(world, (1 << 20) + 17, np.dtype("float32"), 903 + qi)
+                mine = inputs[ring.position]
+                buf = torch.from_numpy(mine.copy()).to(dev)
+                t = ring.all_reduce_async(buf, "avg", quantize=quant)
+                if rank == world - 1:
+                    ring.signal_abort(t.attempt)
+                try:
+                    ring.await_reduce(t)
+                    outcome = "completed"
+                except CollectiveAborted:
+                    outcome = "aborted"
+                outs = [None] * world
+                dist.all_gather_object(outs, outcome)
+                check(f"mid-op abort q={quant}: same outcome everywhere", len(set(outs)) == 1, outs)
+                want = mine if outcome == "aborted" else oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.AVG, quant)
+                check(f"mid-op abort q={quant}: bytes ({outcome})", buf.cpu().numpy().tobytes() == want.tobytes())
             # non-finite under quantization: everyone aborts and restores
             inputs = ring_inputs(world, n, np.dtype("float32"), 901)
             inputs[world // 2][77] = np.inf
@@ -147,8 +168,10 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                 ring.run_all_reduce(view, op, quantize=quant)
                 want = oring.ring_allreduce_chunkwise([x[:cnt] for x in inputs], oring.ReduceOp[op.upper()], quantize=quant)
                 check(f"registered off={lo_off} n={cnt} q={quant} {op}", view.cpu().numpy().tobytes() == want.tobytes())
-            # abort atomicity in zero-copy mode
-            for k in range(2):
+            # abort atomicity in zero-copy mode: barriers 0, 1 and the completion
+            # vote (2), which also waits until every peer's pushes into this
+            # rank's buffer landed before the restore
+            for k in range(3):
                 view = reg[:n]
                 mine = inputs[ring.position]
                 view.copy_(torch.from_numpy(mine))
