@@ -98,7 +98,7 @@ def select_sync_plan(reports: dict[int, tuple[SyncStrategy, list[tuple[str, int,
     (master.py:909-976) without a committed floor: send-only peers are the
     only donors if any exist, receive-only peers never donate, the highest
     revision wins, then the most popular hash (ties: smallest hash, then
-    smallest peer). reports[peer] = (strategy, [(key, revision, hash, nbytes)]).
+    smallest peer). reports[peer] = (strategy, [(key, revision, hash, nbytes, dtype)]).
     Returns {peer: [(key, donor, revision, hash)]} or an error string."""
     send_only = {p for p, (s, _) in reports.items() if s is SyncStrategy.SEND_ONLY}
     recv_only = {p for p, (s, _) in reports.items() if s is SyncStrategy.RECEIVE_ONLY}
@@ -232,7 +232,8 @@ class Communicator:
         self.stats["sync_calls"] += 1
         torch.cuda.synchronize(self.device)
         hashes = simplehash_many([e.buffer for e in entries])  # HASH #1
-        metas = [(e.key, e.revision, h, e.nbytes) for e, h in zip(entries, hashes)]
+        # (key, revision, hash, nbytes, dtype): StateEntryMeta of client.py:705-707
+        metas = [(e.key, e.revision, h, e.nbytes, int(e.dtype)) for e, h in zip(entries, hashes)]
         # entries' IPC handles travel with the report so donors need no second round
         handles = []
         for e in entries:
@@ -243,9 +244,10 @@ class Communicator:
         world = dist.get_world_size(self.group)
         reports: list = [None] * world
         dist.all_gather_object(reports, (strategy.value, metas, handles), group=self.group)
-        keys = [m[0] for m in metas]
-        if any([m[0] for m in r[1]] != keys for r in reports):
-            return SyncOutcomeResult(SyncStatus.ERROR, reason="key sets differ across peers")
+        # the master requires the same (key, dtype, nbytes) from every peer (master.py:712)
+        shape = [(m[0], m[4], m[3]) for m in metas]
+        if any([(m[0], m[4], m[3]) for m in r[1]] != shape for r in reports):
+            return SyncOutcomeResult(SyncStatus.ERROR, reason="entry keys, dtypes or sizes differ across peers")
         if all(r[1] == reports[0][1] for r in reports):
             return SyncOutcomeResult(SyncStatus.IN_SYNC)  # no payload moves (SPEC no-op bandwidth)
         plan = select_sync_plan({p: (SyncStrategy(r[0]), r[1]) for p, r in enumerate(reports)})
@@ -259,6 +261,13 @@ class Communicator:
         try:
             for key, donor, rev, want in plan[me]:
                 i, e = by_key[key]
+                # client.py:750-757: never downgrade, never copy a different size
+                if rev < e.revision:
+                    ok, reason = False, f"plan would downgrade {key!r} from revision {e.revision} to {rev}"
+                    break
+                if reports[donor][1][i][3] != e.nbytes:
+                    ok, reason = False, f"size mismatch for {key!r}"
+                    break
                 h64, off = reports[donor][2][i]
                 ptr = ctypes.c_void_p()
                 check(lib().pcclb_ipc_open(ctypes.create_string_buffer(h64, 64), ctypes.byref(ptr)), "ipc_open")

@@ -128,6 +128,13 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             check("newcomer: updated", res.status is SyncStatus.UPDATED, res)
             check("newcomer: state", [osh.simplehash_c(e.buffer.cpu().numpy()) for e in entries] == ref)
             check("newcomer: revision", all(e.revision == 7 for e in entries))
+            # one peer's entry has another size under the same key: every peer
+            # reports an error and nobody copies (master.py:712, client.py:750-757)
+            n_odd = 4096 + (64 if rank == 0 else 0)
+            odd = torch.zeros(n_odd, dtype=torch.uint8, device=dev) + rank
+            res = comm.sync_shared_state([SharedStateEntry("odd", DType.U8, odd, revision=1 + rank)])
+            check("size mismatch: error", res.status is SyncStatus.ERROR, res)
+            check("size mismatch: untouched", bool((odd == rank).all()))
             comm.close()
 
         if "churn" in scenarios and world >= 3:
