@@ -251,6 +251,71 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                 hs = [None] * world
                 dist.all_gather_object(hs, _hash(buf))
                 check(f"large q={quant}: identical on all ranks", len(set(hs)) == 1)
+        for sc in scenarios:
+            if not sc.startswith("death_"):
+                continue
+            # a peer process dies while the attempt runs (its kernels in flight,
+            # its workspace mapped by the survivors): the survivors end the
+            # attempt the same way (aborted with their bytes back, or completed
+            # if the victim's vote landed first), keep a healthy CUDA context,
+            # and retry at W-1 on a new ring (test_cluster.py:256-307)
+            import time
+
+            quant = sc == "death_quant"
+            victim = world - 1
+            survivors = [r for r in range(world) if r != victim]
+            sub = dist.new_group(survivors, backend="gloo")  # before anyone dies
+            n = 300_000_007
+            eng = DeviceRing(device=dev, capacity_bytes=DeviceRing.required_bytes(n, world, 4, quant), timeout_s=5.0)
+            g = torch.Generator(device=dev).manual_seed(60 + rank)
+            src = torch.randn(n, generator=g, device=dev) * (1e-2 if quant else 1.0)
+            buf = src.clone()
+            torch.cuda.synchronize()
+            dist.barrier()
+            if rank == 0:
+                # the victim arrives at barrier 0 (its token is visible to every
+                # peer) and spins there; it dies before this rank arrives, so the
+                # others pass the barrier and then read the dead rank's workspace
+                time.sleep(0.5)
+            t = eng.all_reduce_async(buf, "sum", quantize=quant)
+            if rank == victim:
+                time.sleep(0.05)
+                with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+                    json.dump(out, f)
+                os._exit(0)  # no cleanup: the context dies with the kernels in flight
+            try:
+                eng.await_reduce(t)
+                outcome = "completed"
+            except CollectiveAborted:
+                outcome = "aborted"
+            outs = [None] * len(survivors)
+            dist.all_gather_object(outs, outcome, group=sub)
+            check(f"{sc}: survivors agree ({outs})", len(set(outs)) == 1, outs)
+            if outcome == "aborted":
+                check(f"{sc}: restored", bool(torch.equal(buf, src)))
+            # the context is healthy: new work runs and the old engine closes
+            x = torch.arange(1000, device=dev, dtype=torch.float64).sum().item()
+            check(f"{sc}: context healthy", x == 499500.0, x)
+            try:
+                eng.close()
+            except Exception as exc:  # noqa: BLE001
+                check(f"{sc}: old engine closes", False, exc)
+            # retry at W-1 on a new ring over the survivors, bit-exact
+            buf.copy_(src)
+            m = 1_000_003
+            part = buf[:m]
+            eng2 = DeviceRing(group=sub, device=dev, capacity_bytes=64 << 20, timeout_s=20.0)
+            eng2.run_all_reduce(part, "sum", quantize=quant)
+            ins = []
+            for r_ in survivors:
+                g2 = torch.Generator(device=dev).manual_seed(60 + r_)
+                ins.append((torch.randn(n, generator=g2, device=dev) * (1e-2 if quant else 1.0))[:m].cpu().numpy())
+            want = oring.ring_allreduce_chunkwise(ins, oring.ReduceOp.SUM, quantize=quant)
+            check(f"{sc}: retry at W-1 exact", part.cpu().numpy().tobytes() == want.tobytes())
+            eng2.close()
+            with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+                json.dump(out, f)
+            os._exit(0)  # the default group has a dead member: skip its teardown
         if "config" in scenarios:
             # BASELINE config sizes; inputs generated on the device from per-rank
             # seeds, so any rank can regenerate a peer's chunk for the oracle

@@ -60,3 +60,26 @@ def test_nvlink_ring(world, tmp_path):
         failures += [(r, c["name"], c["detail"]) for c in res["checks"] if not c["ok"]]
     assert total > 0
     assert not failures, failures[:20]
+
+
+@pytest.mark.parametrize("kind", ["death_plain", "death_quant"])
+def test_peer_death_mid_op(kind, tmp_path):
+    """W=3: one rank's process exits while its kernels run and its workspace
+    is mapped by the others (legacy CUDA IPC); survivors agree on the outcome,
+    restore, keep a healthy context and retry at W=2."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    world = 3
+    cmd = [sys.executable, os.path.join(ROOT, "tests", "mp_ring_worker.py"), str(world), str(_free_port()),
+           str(tmp_path), kind]
+    proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-4000:]
+    failures, total = [], 0
+    for r in range(world - 1):
+        with open(tmp_path / f"rank{r}.json") as f:
+            res = json.load(f)
+        assert not res["errors"], res["errors"][0]
+        total += len(res["checks"])
+        failures += [(r, c["name"], c["detail"]) for c in res["checks"] if not c["ok"]]
+    assert total > 0
+    assert not failures, failures[:20]
