@@ -479,6 +479,67 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     return result
 
 
+def bench_sweep(args, rank, world, local):
+    """Config 2's bandwidth sweep: in-place AVG all-reduce of S = 1 MiB .. 4 GiB
+    fp32 per GPU (x4 steps), K ops back to back per size (CUDA events, max over
+    ranks), registered buffer. value = busbw at 1 GiB."""
+    import torch
+
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
+
+    dev = torch.device("cuda", local)
+    sizes = [1 << e for e in range(20, 33, 2)]  # bytes: 1 MiB, 4 MiB, ..., 4 GiB
+    nmax = sizes[-1] // 4
+    g = torch.Generator(device=dev).manual_seed(rank)
+    src = torch.randn(nmax, generator=g, device=dev)
+    buf = torch.empty_like(src)
+    ring = DeviceRing(device=dev, capacity_bytes=DeviceRing.required_bytes(nmax, world, 4, False))
+    ring.register(buf)
+    stream = torch.cuda.current_stream(dev)
+    rows = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    for S in sizes:
+        n = S // 4
+        view = buf[:n]
+        view.copy_(src[:n])
+        steps = max(5, min(200, (64 << 20) // S * 5))
+        for _ in range(max(3, args.warmup)):
+            ring.run_all_reduce(view, "avg")
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        tickets = []
+        for _ in range(steps):
+            if len(tickets) >= 32:
+                ring.await_reduce(tickets.pop(0))
+            tickets.append(ring.all_reduce_async(view, "avg"))
+        e1.record(stream)
+        for t in tickets:
+            ring.await_reduce(t)
+        torch.cuda.synchronize(dev)
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+        algbw = S / (ms * 1e-3) / 1e9
+        busbw = algbw * 2 * (world - 1) / world if world > 1 else 0.0
+        rows.append({"bytes": S, "us_per_op": round(ms * 1e3, 2), "algbw_GBps": round(algbw, 1),
+                     "busbw_GBps": round(busbw, 1), "frac_of_770": round(busbw / NVLINK_PEER_GBS, 4),
+                     "frac_of_900": round(busbw / 900.0, 4), "ops": steps})
+    clk = clocks.stop()
+    ring.close()
+    at1g = next(r for r in rows if r["bytes"] == 1 << 30)
+    return {
+        "value": at1g["busbw_GBps"], "unit": "GB/s", "ms_per_step": round(at1g["us_per_op"] / 1e3, 4),
+        "scaling": "weak", "dtype": "f32",
+        "config": {"workload": f"config2 sweep: AVG all-reduce of 1 MiB..4 GiB fp32 per GPU, W={world}, registered buffer",
+                   "busbw_definition": "algbw*2(W-1)/W", "sweep": rows},
+        "roofline": {"bound": "nvlink", "achieved": round(at1g["busbw_GBps"], 1), "peak": NVLINK_PEER_GBS,
+                     "unit": "GB/s", "frac": at1g["frac_of_770"], "traffic": None,
+                     "peak_src": "measured peer copy 770 GB/s per direction (B200_PROFILING.md); nominal 900"},
+        "clocks": clk, "e2e": None, "gpu_launches": None,
+    }
+
+
 def bench_local(args, rank, world, local):
     import torch
 
@@ -639,7 +700,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "async", "local"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "hash", "allreduce", "quant", "async", "local", "sweep"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--elems", type=int, default=0, help="override elements per GPU (allreduce/quant/local)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -669,6 +730,8 @@ def main():
         res = bench_allreduce(args, rank, world, local, quantize=True)
     elif workload == "async":
         res = bench_async(args, rank, world, local)
+    elif workload == "sweep":
+        res = bench_sweep(args, rank, world, local)
     else:
         res = bench_local(args, rank, world, local)
     line = {"metric": METRIC, "value": res.pop("value"), "unit": res.pop("unit"), "n_gpus": world,

@@ -190,6 +190,12 @@ PCCLB_API volatile uint64_t *pcclb_ring_abort_word(pcclb_ring *r);
  * takes at most its share of the SM's CTA slots; with more engines than slots
  * the engine falls back to one barrier per ring step. */
 PCCLB_API int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots);
+/* Plain ops of at most `bytes` run as one fused kernel (copy-in, arrival,
+ * local fold of every chunk in its ring order, completion vote): the
+ * latency-bound end of the config-2 sweep. Default 4 MiB (PCCLB_SMALL_MAX
+ * overrides); 0 disables. Every rank of a ring must use the same value (the
+ * path is part of the parameter check at the arrival). */
+PCCLB_API int pcclb_ring_set_small_max(pcclb_ring *r, uint64_t bytes);
 /* Workspace bytes an n-element op needs at this world size (host-only, no
  * GPU needed): the capacity_bytes to pass to pcclb_ring_create. 0 if invalid. */
 PCCLB_API uint64_t pcclb_ring_workspace_bytes(uint64_t n, uint32_t world, int dtype, int quantize);

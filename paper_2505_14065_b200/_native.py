@@ -99,6 +99,7 @@ SIGNATURES = {
     "pcclb_ring_abort_word": (ctypes.POINTER(ctypes.c_uint64), [_P]),
     "pcclb_ring_capacity": (_U64, [_P, _I, _I]),
     "pcclb_ring_set_slots": (_I, [_P, _U32]),
+    "pcclb_ring_set_small_max": (_I, [_P, _U64]),
     "pcclb_ring_workspace_bytes": (_U64, [_U64, _U32, _I, _I]),
     "pcclb_ring_allreduce": (
         _I,

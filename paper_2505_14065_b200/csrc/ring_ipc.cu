@@ -98,6 +98,8 @@ struct Signal {
   pcclb_qmeta gmeta[kIpcMaxWorld];      // written by chunk c's owner: meta of its final codes
   uint64_t vote[kIpcMaxWorld];          // coordinator only: peer j's completion vote (attempt << 8 | failed)
   uint64_t decision;                    // written by the coordinator: attempt << 8 | 1 commit / 2 abort
+  uint64_t small_copied;                // small path: attempt << 8 | 1 copied in + arrived / 2 failed
+  uint32_t small_ctr[2];                // small path: CTAs done copying / folding (reset by the last CTA)
 };
 static_assert(sizeof(Signal) <= kSignalBytes, "signal area too small");
 
@@ -236,8 +238,13 @@ struct VoteArgs {
   uint32_t fault;  // 1: inject a local failure at the vote
 };
 
+__device__ void vote_thread0(const VoteArgs &a);
+
 __global__ void __launch_bounds__(32) ipc_vote_kernel(const __grid_constant__ VoteArgs a) {
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x == 0) vote_thread0(a);
+}
+
+__device__ void vote_thread0(const VoteArgs &a) {
   Signal *me = a.mine;
   uint32_t st = *(volatile uint32_t *)&me->status;
   if (st == 0 && a.fault) st = PCCLB_EIO;
@@ -425,6 +432,142 @@ __global__ void __launch_bounds__(kFoldThreads) ipc_fold_kernel(const __grid_con
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// small messages (plain ops): the whole attempt in one kernel
+// ---------------------------------------------------------------------------
+// For short buffers the attempt is latency-bound: every kernel boundary and
+// barrier costs microseconds. One kernel of G co-resident CTAs copies the
+// caller's buffer into `in`, arrives (the last CTA to finish copying posts
+// the arrival token and the parameter descriptor to every peer), waits for
+// every peer's arrival, folds EVERY chunk locally from the W inputs (W-1 read
+// over NVLink) in its ring order x_c, x_{c+1}, ..., x_{c-1} -- the same values
+// as the owner's fold, with (W-1)*N instead of 2(W-1)/W*N ingress, which does
+// not matter at these sizes -- and the last CTA to finish folding runs the
+// completion vote and, on a failed attempt, the restore. Abort points:
+// fault_at 0/1 at the arrival, 2 at the vote.
+template <typename T>
+struct SmallArgs {
+  T *buf;                         // caller buffer (written with the result)
+  T *in;                          // this rank's workspace copy (read by peers)
+  const T *pin[kIpcMaxWorld];     // input of ring position p (pin[rank] = in)
+  uint64_t lo[kIpcMaxWorld + 1];  // chunk bounds
+  uint64_t n;
+  VoteArgs v;                     // mine, peers, host, attempt, timeout, rank, world, coord, fault (vote)
+  uint64_t desc;
+  uint32_t fault_arrive;
+  uint32_t avg;
+};
+
+// copy over CTAs [cta, cta + nctas): 16-byte vectors when both sides share
+// their offset modulo 16, else 4-byte words (f32/f64 buffers)
+__device__ __forceinline__ void cta_copy_any(const void *src, void *dst, uint64_t bytes, uint32_t cta,
+                                             uint32_t nctas) {
+  if (((reinterpret_cast<uintptr_t>(src) ^ reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    cta_range_copy(src, dst, bytes, cta, nctas);
+    return;
+  }
+  const uint32_t *s4 = static_cast<const uint32_t *>(src);
+  uint32_t *d4 = static_cast<uint32_t *>(dst);
+  const uint64_t tid = (uint64_t)cta * blockDim.x + threadIdx.x, nth = (uint64_t)nctas * blockDim.x;
+  for (uint64_t i = tid; i < bytes / 4; i += nth) d4[i] = s4[i];
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kIpcThreads) ipc_small_kernel(const __grid_constant__ SmallArgs<T> a) {
+  __shared__ uint32_t s_flag;
+  Signal *me = a.v.mine;
+  const uint32_t G = gridDim.x, w = a.v.world, rank = a.v.rank;
+  const uint64_t token = a.v.attempt << 8;  // barrier index 0
+  // 1. copy-in (every CTA its share)
+  cta_copy_any(a.buf, a.in, a.n * sizeof(T), blockIdx.x, G);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_flag = atomicAdd(&me->small_ctr[0], 1u) == G - 1;
+  }
+  __syncthreads();
+  if (s_flag && threadIdx.x == 0) {
+    // the last copier arrives for this rank (or aborts instead)
+    uint32_t v = *(volatile uint32_t *)&me->status;
+    if (v == 0 && a.fault_arrive) v = PCCLB_EIO;
+    if (v == 0 && a.v.host->abort >= a.v.attempt) v = PCCLB_EABORTED;
+    if (v) {
+      *(volatile uint32_t *)&me->status = v;
+      for (uint32_t j = 0; j < w; ++j)
+        if (j != rank) st_release_sys(&a.v.peer[j]->abort_tok[rank], a.v.attempt);
+    } else {
+      __threadfence_system();
+      for (uint32_t j = 0; j < w; ++j)
+        if (j != rank) {
+          *(volatile uint64_t *)&a.v.peer[j]->desc[rank] = a.desc;
+          st_release_sys(&a.v.peer[j]->arrive[rank], token);
+        }
+    }
+    __threadfence();
+    *(volatile uint64_t *)&me->small_copied = token | (v ? 2u : 1u);
+  }
+  // 2. every CTA waits for this rank's own arrival and all peers'
+  if (threadIdx.x == 0) {
+    uint32_t verdict = 0;
+    uint64_t c;
+    while (((c = *(volatile uint64_t *)&me->small_copied) >> 8) != a.v.attempt) {
+    }
+    if ((c & 0xff) != 1u) verdict = PCCLB_EABORTED;
+    const uint64_t t0 = globaltimer();
+    while (!verdict) {
+      bool all = true;
+      for (uint32_t j = 0; j < w; ++j) {
+        if (j == rank) continue;
+        if (ld_relaxed_sys(&me->arrive[j]) < token) all = false;
+        if (ld_relaxed_sys(&me->abort_tok[j]) == a.v.attempt) verdict = PCCLB_EABORTED;
+      }
+      if (verdict) break;
+      if (all) {
+        __threadfence_system();  // acquire: the peers' copies are visible
+        for (uint32_t j = 0; j < w; ++j)
+          if (j != rank && *(volatile uint64_t *)&me->desc[j] != a.desc) verdict = PCCLB_EINVAL;
+        break;
+      }
+      if (a.v.host->abort >= a.v.attempt) verdict = PCCLB_EABORTED;
+      else if (globaltimer() - t0 > a.v.timeout_ns) verdict = PCCLB_ETIMEOUT;
+    }
+    if (verdict) {
+      atomicCAS(&me->status, 0u, verdict);
+      for (uint32_t j = 0; j < w; ++j)
+        if (j != rank) st_release_sys(&a.v.peer[j]->abort_tok[rank], a.v.attempt);
+    }
+    s_flag = verdict == 0;
+  }
+  __syncthreads();
+  // 3. fold every chunk in its ring order
+  if (s_flag) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (uint64_t)G * blockDim.x;
+    for (uint32_t c = 0; c < w; ++c) {
+      const uint64_t c0 = a.lo[c], c1 = a.lo[c + 1];
+      for (uint64_t i = c0 + tid; i < c1; i += nth) {
+        T acc = a.pin[c][i];
+        for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.pin[(c + k) % w][i], acc);
+        a.buf[i] = a.avg ? div_world(acc, (T)a.avg) : acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_flag = atomicAdd(&me->small_ctr[1], 1u) == G - 1;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  // 4. the last CTA: completion vote, then the restore of a failed attempt
+  if (threadIdx.x == 0) vote_thread0(a.v);
+  __syncthreads();
+  if (op_failed(me)) cta_copy_any(a.in, a.buf, a.n * sizeof(T), 0, 1);
+  if (threadIdx.x == 0) {
+    me->small_ctr[0] = 0;
+    me->small_ctr[1] = 0;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // gather: W-1 chunk copies (grid.y = job), plain (verbatim) or quantized (dequant)
@@ -1125,6 +1268,7 @@ struct pcclb_ring {
   cudaEvent_t op_events[kMaxOps];
   uint32_t next_ticket = 0;
   uint32_t slots = 2;  // engines that may run ops concurrently on this GPU (pcclb_ring_set_slots)
+  uint64_t small_max = ~0ull;  // plain ops up to this many bytes: one-kernel path (~0: default)
   uint64_t last_n;
   int last_dtype;
   bool have_backup;
@@ -1198,6 +1342,25 @@ int launch_barrier(pcclb_ring *r, uint64_t attempt, uint32_t index, int fault_at
 
 unsigned ipc_grid(uint64_t n_vec, int ctas_per_sm = 4) {
   return grid_for(n_vec, kIpcThreads, ctas_per_sm);
+}
+
+// Plain ops up to this size take the one-kernel small path (ipc_small_kernel).
+// PCCLB_SMALL_MAX (bytes) overrides; 0 disables.
+uint64_t small_max_bytes(const pcclb_ring *r) {
+  if (r->small_max != ~0ull) return r->small_max;  // pcclb_ring_set_small_max
+  static const long long env = [] {
+    const char *e = getenv("PCCLB_SMALL_MAX");
+    return e ? atoll(e) : -1ll;
+  }();
+  if (env >= 0) return (uint64_t)env;
+  return 4ull << 20;
+}
+// co-resident grid (the CTAs wait for each other): one CTA per 64 Ki elements, at most 64
+unsigned small_grid(uint64_t n) {
+  uint64_t g = (n + 65535) / 65536;
+  if (g < 1) g = 1;
+  if (g > 64) g = 64;
+  return (unsigned)g;
 }
 
 // The attempt's last two kernels: completion vote (fault point `index`),
@@ -1311,10 +1474,49 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const uint32_t own = (rank + 1) % w;  // collective.py:538
   const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
   Signal *me = sig_of(r->ws);
+  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : PCCLB_F32, op, false);
+  if (n * sizeof(T) <= small_max_bytes(r)) {
+    // latency-bound size: the whole attempt in one kernel (ipc_small_kernel)
+    r->last_zero_copy = false;
+    SmallArgs<T> a{};
+    a.buf = buf;
+    a.in = reinterpret_cast<T *>(r->ws + L.in);
+    for (uint32_t j = 0; j < w; ++j) a.pin[j] = reinterpret_cast<const T *>(r->peer_ws[j] + L.in);
+    for (uint32_t c = 0; c < w; ++c) a.lo[c] = lo[2 * c];
+    a.lo[w] = n;
+    a.n = n;
+    a.v.mine = me;
+    for (uint32_t j = 0; j < w; ++j) a.v.peer[j] = sig_of(r->peer_ws[j]);
+    a.v.host = r->host_dev;
+    a.v.attempt = attempt;
+    a.v.timeout_ns = timeout_ns;
+    a.v.rank = rank;
+    a.v.world = w;
+    a.v.coord = 0;
+    a.v.fault = (fault_at == 2) ? 1u : 0u;
+    a.fault_arrive = (fault_at == 0 || fault_at == 1) ? 1u : 0u;
+    a.desc = desc | (1ull << 38);  // bit 38: small path (ranks must agree)
+    a.avg = (op == PCCLB_AVG) ? w : 0;
+    const unsigned grid = small_grid(n);
+    r->timer.mark(s);
+    switch (op) {
+      case PCCLB_MAX:
+        ipc_small_kernel<T, PCCLB_MAX><<<grid, kIpcThreads, 0, s>>>(a);
+        break;
+      case PCCLB_MIN:
+        ipc_small_kernel<T, PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(a);
+        break;
+      default:
+        ipc_small_kernel<T, PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(a);
+        break;
+    }
+    PCCLB_LAUNCH_CHECK();
+    r->timer.mark(s);
+    return PCCLB_OK;
+  }
   const int slot = find_reg(r, buf, n * sizeof(T));
   const bool zero_copy = slot >= 0;
   r->last_zero_copy = zero_copy;
-  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : PCCLB_F32, op, false);
   const T *inputs[kIpcMaxWorld];  // where each ring position's input lives
   r->timer.mark(s);
   if (zero_copy) {
@@ -1777,6 +1979,12 @@ int pcclb_ring_import(pcclb_ring *r, uint32_t peer, const void *handle64) {
 uint64_t pcclb_ring_workspace_bytes(uint64_t n, uint32_t world, int dtype, int quantize) {
   if (world < 1 || world > (uint32_t)kIpcMaxWorld || !valid_dtype(dtype)) return 0;
   return layout_for(n, world, dtype_size(dtype), quantize != 0).end;
+}
+
+int pcclb_ring_set_small_max(pcclb_ring *r, uint64_t bytes) {
+  if (!r) return PCCLB_EINVAL;
+  r->small_max = bytes;
+  return PCCLB_OK;
 }
 
 int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots) {

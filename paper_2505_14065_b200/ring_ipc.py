@@ -65,7 +65,8 @@ class DeviceRing:
     """
 
     def __init__(self, group=None, ring: list[int] | None = None, device=None,
-                 capacity_bytes: int = 64 << 20, timeout_s: float = 60.0, slots: int = 2):
+                 capacity_bytes: int = 64 << 20, timeout_s: float = 60.0, slots: int = 2,
+                 small_max_bytes: int | None = None):
         if not dist.is_initialized():
             raise UsageError("torch.distributed must be initialized")
         self.group = group
@@ -85,6 +86,8 @@ class DeviceRing:
         self._pending = 0  # enqueued attempts not yet awaited
         # engines sharing this GPU concurrently (the communicator's pool size)
         self.slots = max(1, int(slots))
+        # plain ops up to this size run as one fused kernel (None: library default, 4 MiB)
+        self.small_max_bytes = small_max_bytes
         self._create(capacity_bytes)
 
     # -- workspace lifecycle (collective: every rank calls in the same order) --
@@ -98,6 +101,8 @@ class DeviceRing:
         self._handle = h
         self._capacity = capacity_bytes
         check(lib().pcclb_ring_set_slots(h, self.slots), "ring_set_slots")
+        if self.small_max_bytes is not None:
+            check(lib().pcclb_ring_set_small_max(h, int(self.small_max_bytes)), "ring_set_small_max")
         mine = ctypes.create_string_buffer(64)
         check(lib().pcclb_ring_export(h, mine), "ring_export")
         handles = exchange_bytes(bytes(mine.raw), self.group)  # indexed by group rank

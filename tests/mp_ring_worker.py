@@ -54,13 +54,15 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
         if "golden" in scenarios:
             # every golden case with W == world, in identity and reversed ring order
             rev = DeviceRing(device=dev, ring=list(reversed(range(world))), capacity_bytes=64 << 20, timeout_s=20.0)
+            # the same cases on the multi-kernel schedule (small path off)
+            big = DeviceRing(device=dev, capacity_bytes=64 << 20, timeout_s=20.0, small_max_bytes=0)
             for idx, case in enumerate(RING_CASES):
                 w, n, op, quant, dt, seed = case
                 if w != world:
                     continue
                 want = golden["ring"][idx]["output_hash"]
                 inputs = ring_inputs(w, n, np.dtype(dt), seed)
-                for eng, tag in ((ring, "id"), (rev, "rev")):
+                for eng, tag in ((ring, "id"), (rev, "rev"), (big, "id/multi-kernel")):
                     pos = eng.position
                     buf = torch.from_numpy(inputs[pos].copy()).to(dev)
                     st = eng.run_all_reduce(buf, op, quantize=quant)
@@ -346,6 +348,7 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
         ring.close()
         if rev is not None:
             rev.close()
+            big.close()
     except Exception:  # noqa: BLE001
         out["errors"].append(traceback.format_exc())
     with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
