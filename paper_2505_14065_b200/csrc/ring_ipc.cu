@@ -99,6 +99,7 @@ struct Signal {
   uint64_t vote[kIpcMaxWorld];          // coordinator only: peer j's completion vote (attempt << 8 | failed)
   uint64_t decision;                    // written by the coordinator: attempt << 8 | 1 commit / 2 abort
   uint64_t small_copied;                // small path: attempt << 8 | 1 copied in + arrived / 2 failed
+  uint64_t small_go;                    // small path: attempt << 8 | 1 every peer arrived / 2 failed
   uint32_t small_ctr[2];                // small path: CTAs done copying / folding (reset by the last CTA)
 };
 static_assert(sizeof(Signal) <= kSignalBytes, "signal area too small");
@@ -457,6 +458,7 @@ struct SmallArgs {
   uint64_t desc;
   uint32_t fault_arrive;
   uint32_t avg;
+  uint32_t *status_out;           // host-mapped: the attempt's final status
 };
 
 // copy over CTAs [cta, cta + nctas): 16-byte vectors when both sides share
@@ -479,6 +481,7 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_small_kernel(const __grid_con
   Signal *me = a.v.mine;
   const uint32_t G = gridDim.x, w = a.v.world, rank = a.v.rank;
   const uint64_t token = a.v.attempt << 8;  // barrier index 0
+  if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile uint32_t *)&me->status = 0u;  // read after the copy counter
   // 1. copy-in (every CTA its share)
   cta_copy_any(a.buf, a.in, a.n * sizeof(T), blockIdx.x, G);
   __syncthreads();
@@ -507,15 +510,17 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_small_kernel(const __grid_con
     __threadfence();
     *(volatile uint64_t *)&me->small_copied = token | (v ? 2u : 1u);
   }
-  // 2. every CTA waits for this rank's own arrival and all peers'
-  if (threadIdx.x == 0) {
+  // 2. CTA 0 waits for this rank's own arrival and every peer's (host abort
+  // and timeout polled there only), then releases the other CTAs through a
+  // local flag
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     uint32_t verdict = 0;
     uint64_t c;
     while (((c = *(volatile uint64_t *)&me->small_copied) >> 8) != a.v.attempt) {
     }
     if ((c & 0xff) != 1u) verdict = PCCLB_EABORTED;
     const uint64_t t0 = globaltimer();
-    while (!verdict) {
+    for (uint32_t spin = 0; !verdict; ++spin) {
       bool all = true;
       for (uint32_t j = 0; j < w; ++j) {
         if (j == rank) continue;
@@ -529,26 +534,73 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_small_kernel(const __grid_con
           if (j != rank && *(volatile uint64_t *)&me->desc[j] != a.desc) verdict = PCCLB_EINVAL;
         break;
       }
-      if (a.v.host->abort >= a.v.attempt) verdict = PCCLB_EABORTED;
-      else if (globaltimer() - t0 > a.v.timeout_ns) verdict = PCCLB_ETIMEOUT;
+      if ((spin & 63) == 63) {  // host memory and the clock: every 64 polls
+        if (a.v.host->abort >= a.v.attempt) verdict = PCCLB_EABORTED;
+        else if (globaltimer() - t0 > a.v.timeout_ns) verdict = PCCLB_ETIMEOUT;
+      }
     }
     if (verdict) {
       atomicCAS(&me->status, 0u, verdict);
       for (uint32_t j = 0; j < w; ++j)
         if (j != rank) st_release_sys(&a.v.peer[j]->abort_tok[rank], a.v.attempt);
     }
-    s_flag = verdict == 0;
+    __threadfence();
+    *(volatile uint64_t *)&me->small_go = token | (verdict ? 2u : 1u);
+  }
+  if (threadIdx.x == 0) {
+    uint64_t gv;
+    while (((gv = *(volatile uint64_t *)&me->small_go) >> 8) != a.v.attempt) __nanosleep(20);
+    s_flag = (gv & 0xff) == 1u;
+    __threadfence();
   }
   __syncthreads();
-  // 3. fold every chunk in its ring order
+  // 3. fold every chunk in its ring order: 16-byte loads of every input (the
+  // workspaces are 16-byte aligned), U vectors per thread in flight
   if (s_flag) {
+    constexpr int N = Pack16<T>::N, U = 4;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (uint64_t)G * blockDim.x;
+    const bool vst = (reinterpret_cast<uintptr_t>(a.buf) & 15) == 0;
+    auto fin = [&](T v) { return a.avg ? div_world(v, (T)a.avg) : v; };
     for (uint32_t c = 0; c < w; ++c) {
       const uint64_t c0 = a.lo[c], c1 = a.lo[c + 1];
-      for (uint64_t i = c0 + tid; i < c1; i += nth) {
-        T acc = a.pin[c][i];
-        for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(a.pin[(c + k) % w][i], acc);
-        a.buf[i] = a.avg ? div_world(acc, (T)a.avg) : acc;
+      auto src = [&](uint32_t k) { return a.pin[c + k < w ? c + k : c + k - w]; };
+      auto one = [&](uint64_t i) {
+        T acc = src(0)[i];
+        for (uint32_t k = 1; k < w; ++k) acc = reduce_op<OP>(src(k)[i], acc);
+        a.buf[i] = fin(acc);
+      };
+      uint64_t v0 = (c0 + N - 1) / N, v1 = c1 / N;
+      if (v1 < v0) v1 = v0;
+      for (uint64_t i = c0 + tid; i < c1 && i < v0 * N; i += nth) one(i);  // head
+      for (uint64_t i = v1 * N + tid; i < c1; i += nth)                     // tail
+        if (i >= v0 * N) one(i);
+      for (uint64_t vb = v0 + tid; vb < v1; vb += nth * U) {
+        Pack16<T> acc[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (vb + u * nth < v1) acc[u] = ld16(src(0) + (vb + u * nth) * N);
+        for (uint32_t k = 1; k < w; ++k) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (vb + u * nth < v1) x[u] = ld16(src(k) + (vb + u * nth) * N);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < N; ++e) acc[u].e[e] = reduce_op<OP>(x[u].e[e], acc[u].e[e]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (vb + u * nth >= v1) continue;
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc[u].e[e] = fin(acc[u].e[e]);
+          T *d = a.buf + (vb + u * nth) * N;
+          if (vst) {
+            st16(d, acc[u]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < N; ++e) d[e] = acc[u].e[e];
+          }
+        }
       }
     }
   }
@@ -563,9 +615,12 @@ __global__ void __launch_bounds__(kIpcThreads) ipc_small_kernel(const __grid_con
   if (threadIdx.x == 0) vote_thread0(a.v);
   __syncthreads();
   if (op_failed(me)) cta_copy_any(a.in, a.buf, a.n * sizeof(T), 0, 1);
+  __syncthreads();
   if (threadIdx.x == 0) {
     me->small_ctr[0] = 0;
     me->small_ctr[1] = 0;
+    __threadfence_system();
+    *(volatile uint32_t *)a.status_out = *(volatile uint32_t *)&me->status;
   }
 }
 
@@ -1263,7 +1318,9 @@ struct pcclb_ring {
   bool imported[kIpcMaxWorld];
   HostFlags *host;                 // host-mapped
   HostFlags *host_dev;             // device alias
-  uint32_t *status_host;           // pinned status readback, one slot per op record
+  uint32_t *status_host;           // pinned status readback, one slot per op record (host-mapped)
+  uint32_t *status_dev;            // device alias of status_host
+  uint32_t *cur_status_dev = nullptr;  // the slot of the op being enqueued (small path writes it)
   OpRec ops[kMaxOps];
   cudaEvent_t op_events[kMaxOps];
   uint32_t next_ticket = 0;
@@ -1353,13 +1410,16 @@ uint64_t small_max_bytes(const pcclb_ring *r) {
     return e ? atoll(e) : -1ll;
   }();
   if (env >= 0) return (uint64_t)env;
-  return 4ull << 20;
+  // the small path's NVLink ingress is (W-1)*N against the ring's 2(W-1)/W*N:
+  // equal at W=2, W/2 times more beyond (W=2 measured: 1 MiB 29.9 vs 55.6 us,
+  // 4 MiB 33.2 vs 62.2 us on the multi-kernel schedule)
+  return (32ull << 20) / (r->world ? r->world : 1);
 }
-// co-resident grid (the CTAs wait for each other): one CTA per 64 Ki elements, at most 64
+// co-resident grid (the CTAs wait for each other): one CTA per 8 Ki elements, at most 128
 unsigned small_grid(uint64_t n) {
-  uint64_t g = (n + 65535) / 65536;
+  uint64_t g = (n + 8191) / 8192;
   if (g < 1) g = 1;
-  if (g > 64) g = 64;
+  if (g > 128) g = 128;
   return (unsigned)g;
 }
 
@@ -1497,6 +1557,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
     a.fault_arrive = (fault_at == 0 || fault_at == 1) ? 1u : 0u;
     a.desc = desc | (1ull << 38);  // bit 38: small path (ranks must agree)
     a.avg = (op == PCCLB_AVG) ? w : 0;
+    a.status_out = r->cur_status_dev;
     const unsigned grid = small_grid(n);
     r->timer.mark(s);
     switch (op) {
@@ -1929,7 +1990,8 @@ int pcclb_ring_create(int device, uint32_t rank, uint32_t world, uint64_t capaci
   e = cudaMemset(r->ws, 0, kSignalBytes);
   if (e == cudaSuccess) e = cudaHostAlloc(&r->host, sizeof(HostFlags), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->host_dev, r->host, 0);
-  if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, sizeof(uint32_t) * kMaxOps, cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->status_host, sizeof(uint32_t) * kMaxOps, cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&r->status_dev, r->status_host, 0);
   for (int i = 0; i < kMaxOps && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(&r->op_events[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -2039,7 +2101,11 @@ int pcclb_ring_enqueue(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op
   } else {
     Signal *me = sig_of(r->ws);
     r->timer.n = 0;
-    PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
+    // the one-kernel small path resets the status word and hands its outcome to
+    // the host itself (status_dev); the other schedules use a memset and a copy
+    const bool small = !quantize && n * esz <= small_max_bytes(r);
+    r->cur_status_dev = small ? &r->status_dev[t] : nullptr;
+    if (!small) PCCLB_CUDA(cudaMemsetAsync(&me->status, 0, sizeof(uint32_t), s));
     const uint64_t timeout_ns = (uint64_t)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
     int rc;
     if (quantize)
@@ -2050,7 +2116,8 @@ int pcclb_ring_enqueue(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op
       rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
     if (rc) return rc;
     o.zero_copy = !quantize && r->last_zero_copy;
-    PCCLB_CUDA(cudaMemcpyAsync(&r->status_host[t], &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (!small)
+      PCCLB_CUDA(cudaMemcpyAsync(&r->status_host[t], &me->status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   }
   PCCLB_CUDA(cudaEventRecord(o.done, s));
   o.pending = true;
