@@ -70,12 +70,27 @@ class ClockSampler:
     }
 
     def __init__(self, index: int, period: float = 0.1):
+        """NVML is initialised here, before warm-up: on a fresh box nvmlInit
+        takes long and holds driver locks, which stalled the first timed
+        all-reduces of a run (2.5 -> 3.5-4.7 ms at W=4)."""
         self.index = index
         self.period = period
         self.samples = []
         self.stop_ev = threading.Event()
         self.thread = None
         self.h = None
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self.samples.clear()
+        except Exception:  # noqa: BLE001
+            self.h = None
 
     def _sample(self):
         import pynvml
@@ -88,18 +103,9 @@ class ClockSampler:
         self.samples.append((sm, bits))
 
     def start(self):
-        if os.environ.get("BENCH_NO_CLOCKS"):
+        if self.h is None:
             return
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self._sample()
-        except Exception:  # noqa: BLE001
-            self.h = None
-            return
+        self._sample()
 
         def loop():
             while not self.stop_ev.wait(self.period):
@@ -192,6 +198,7 @@ def bench_hash(args, rank, world, local):
     from paper_2505_14065_b200.sharedstate import simplehash_many_async
 
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)  # NVML initialised before warm-up
     layout = llama3_8b_layout()
     total_elems = sum(n for _, n in layout)
     state = torch.empty(total_elems, dtype=torch.bfloat16, device=dev)
@@ -209,7 +216,6 @@ def bench_hash(args, rank, world, local):
         simplehash_many_async(views, out)
     torch.cuda.synchronize(dev)
     barrier(world)
-    clocks = ClockSampler(local)
     clocks.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -340,6 +346,7 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     from paper_2505_14065_b200.ring_ipc import DeviceRing
 
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)  # NVML initialised before warm-up
     n = args.elems or ((1 << 28) if not quantize else 1_200_000_000)
     op = "avg"
     g = torch.Generator(device=dev).manual_seed(rank)
@@ -360,7 +367,6 @@ def bench_allreduce(args, rank, world, local, quantize=False):
     buf.copy_(src)
     torch.cuda.synchronize(dev)
     barrier(world)
-    clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -488,6 +494,7 @@ def bench_sweep(args, rank, world, local):
     from paper_2505_14065_b200.ring_ipc import DeviceRing
 
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)  # NVML initialised before warm-up
     sizes = [1 << e for e in range(20, 33, 2)]  # bytes: 1 MiB, 4 MiB, ..., 4 GiB
     nmax = sizes[-1] // 4
     g = torch.Generator(device=dev).manual_seed(rank)
@@ -497,7 +504,6 @@ def bench_sweep(args, rank, world, local):
     ring.register(buf)
     stream = torch.cuda.current_stream(dev)
     rows = []
-    clocks = ClockSampler(local)
     clocks.start()
     for S in sizes:
         n = S // 4
@@ -546,6 +552,7 @@ def bench_local(args, rank, world, local):
     from paper_2505_14065_b200 import LocalRing
 
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)  # NVML initialised before warm-up
     w = 8
     n = args.elems or (1 << 28)
     g = torch.Generator(device=dev).manual_seed(0)
@@ -556,7 +563,6 @@ def bench_local(args, rank, world, local):
     for _ in range(args.warmup):
         ring.launch(bufs, "avg")
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -592,6 +598,7 @@ def bench_async(args, rank, world, local):
     from paper_2505_14065_b200.ring_ipc import DeviceRing
 
     dev = torch.device("cuda", local)
+    clocks = ClockSampler(local)  # NVML initialised before warm-up
     torch.cuda.set_device(dev)
     n = args.elems or 600_000_000
     g = torch.Generator(device=dev).manual_seed(rank)
@@ -610,7 +617,6 @@ def bench_async(args, rank, world, local):
         step()
     torch.cuda.synchronize(dev)
     barrier(world)
-    clocks = ClockSampler(local)
     clocks.start()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
