@@ -50,6 +50,10 @@ typedef enum {
 enum { PCCLB_F32 = 1, PCCLB_F64 = 2 };
 /* wire.py:141-145 ReduceOpCode; collective.py:43-71 ReduceOp/_ACCUMULATE */
 enum { PCCLB_SUM = 1, PCCLB_AVG = 2, PCCLB_MAX = 3, PCCLB_MIN = 4 };
+/* Extension (north_star; absent from the reference, wire.py:141-145, so its
+ * parity is unpinned): PROD folds with np.multiply in the same ring order.
+ * Not sent over the reference's TCP frames (off-box peers reject it). */
+enum { PCCLB_PROD = 5 };
 
 /* Span range accumulator for quantization (collective.py:117-121).
  * Order-preserving u32 keys so device atomics can reduce min/max; all-zero

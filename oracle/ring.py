@@ -33,6 +33,10 @@ class ReduceOp(IntEnum):
     AVG = 2
     MAX = 3
     MIN = 4
+    # extension op (north_star), not in the reference: PARITY UNPINNED -- its
+    # oracle is this restatement's own definition, np.multiply folded in the
+    # reference's ring order exactly like SUM folds with np.add
+    PROD = 5
 
 
 # collective.py:66-71 -- accumulate(local, incoming, out=local)
@@ -41,6 +45,7 @@ _ACCUMULATE = {
     ReduceOp.AVG: np.add,
     ReduceOp.MAX: np.maximum,
     ReduceOp.MIN: np.minimum,
+    ReduceOp.PROD: np.multiply,
 }
 
 

@@ -44,6 +44,9 @@ class ReduceOp(Enum):
     AVG = "avg"
     MAX = "max"
     MIN = "min"
+    # extension (north_star): np.multiply in the same fold order; not in the
+    # reference's ReduceOpCode (wire.py:141-145), so off-box frames reject it
+    PROD = "prod"
 
     @property
     def code(self) -> int:
@@ -67,7 +70,7 @@ class ReduceOp(Enum):
         return cls.from_code(int(op))
 
 
-_OP_CODE = {ReduceOp.SUM: 1, ReduceOp.AVG: 2, ReduceOp.MAX: 3, ReduceOp.MIN: 4}
+_OP_CODE = {ReduceOp.SUM: 1, ReduceOp.AVG: 2, ReduceOp.MAX: 3, ReduceOp.MIN: 4, ReduceOp.PROD: 5}
 _CODE_OP = {v: k for k, v in _OP_CODE.items()}
 
 DTYPE_CODE = {torch.float32: F32, torch.float64: F64}

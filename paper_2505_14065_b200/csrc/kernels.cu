@@ -79,6 +79,8 @@ static int dispatch_accumulate(void *acc, const void *in, uint64_t n, int op, cu
       return launch_accumulate<T, PCCLB_MAX>(a, b, n, s);
     case PCCLB_MIN:
       return launch_accumulate<T, PCCLB_MIN>(a, b, n, s);
+    case PCCLB_PROD:
+      return launch_accumulate<T, PCCLB_PROD>(a, b, n, s);
   }
   return PCCLB_EINVAL;
 }
@@ -252,6 +254,9 @@ int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint64_t n,
       break;
     case PCCLB_MIN:
       PCCLB_DQA(PCCLB_MIN);
+      break;
+    case PCCLB_PROD:
+      PCCLB_DQA(PCCLB_PROD);
       break;
     default:
       PCCLB_DQA(PCCLB_SUM);

@@ -124,6 +124,8 @@ __device__ __forceinline__ T reduce_op(T local, T incoming) {
     return np_maximum(local, incoming);
   } else if constexpr (OP == PCCLB_MIN) {
     return np_minimum(local, incoming);
+  } else if constexpr (OP == PCCLB_PROD) {
+    return x86_mul(local, incoming);  // np.multiply (extension op)
   } else {
     return x86_add(local, incoming);
   }
@@ -229,6 +231,7 @@ __device__ __forceinline__ float div_world_x(float x, float w) {
 template <int OP, bool X86, typename T>
 __device__ __forceinline__ T reduce_op_x(T local, T incoming) {
   if constexpr (X86 || OP == PCCLB_MAX || OP == PCCLB_MIN) return reduce_op<OP>(local, incoming);
+  else if constexpr (OP == PCCLB_PROD) return FTraits<T>::mul(local, incoming);
   else return FTraits<T>::add(local, incoming);
 }
 

@@ -1567,6 +1567,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
       case PCCLB_MIN:
         ipc_small_kernel<T, PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(a);
         break;
+      case PCCLB_PROD:
+        ipc_small_kernel<T, PCCLB_PROD><<<grid, kIpcThreads, 0, s>>>(a);
+        break;
       default:
         ipc_small_kernel<T, PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(a);
         break;
@@ -1640,6 +1643,9 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
         break;
       case PCCLB_MIN:
         PCCLB_IPC_FOLD(PCCLB_MIN);
+        break;
+      case PCCLB_PROD:
+        PCCLB_IPC_FOLD(PCCLB_PROD);
         break;
       default:
         PCCLB_IPC_FOLD(PCCLB_SUM);
@@ -1833,6 +1839,9 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
         case PCCLB_MIN:
           ipc_qstep_kernel<PCCLB_MIN><<<grid, kQThreads, 0, s>>>(q);
           break;
+        case PCCLB_PROD:
+          ipc_qstep_kernel<PCCLB_PROD><<<grid, kQThreads, 0, s>>>(q);
+          break;
         default:
           ipc_qstep_kernel<PCCLB_SUM><<<grid, kQThreads, 0, s>>>(q);
           break;
@@ -1868,6 +1877,9 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
           break;
         case PCCLB_MIN:
           ipc_dequant_acc_kernel<PCCLB_MIN><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());
+          break;
+        case PCCLB_PROD:
+          ipc_dequant_acc_kernel<PCCLB_PROD><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());
           break;
         default:
           ipc_dequant_acc_kernel<PCCLB_SUM><<<grid, kIpcThreads, 0, s>>>(buf + ra, codes, rn, meta, &me->range[step + 1], bak + ra, me, dqa_mode_value());

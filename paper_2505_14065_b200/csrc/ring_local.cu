@@ -285,6 +285,9 @@ static int local_plain(const LocalBufs<T> &P, int op, bool vec, dim3 grid, cudaS
     case PCCLB_MIN:
       PCCLB_FOLD(PCCLB_MIN);
       break;
+    case PCCLB_PROD:
+      PCCLB_FOLD(PCCLB_PROD);
+      break;
     default:
       PCCLB_FOLD(PCCLB_SUM);
       break;
@@ -356,6 +359,9 @@ int pcclb_local_allreduce(void *const *h_bufs, uint32_t w, uint64_t n, int dtype
         break;
       case PCCLB_MIN:
         local_q_hop_kernel<PCCLB_MIN><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
+        break;
+      case PCCLB_PROD:
+        local_q_hop_kernel<PCCLB_PROD><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
         break;
       default:
         local_q_hop_kernel<PCCLB_SUM><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);

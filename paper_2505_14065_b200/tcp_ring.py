@@ -171,6 +171,8 @@ class TcpRingEngine:
     def run_all_reduce(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,
                        tag: int = 0, seq_nr: int = 1) -> tuple[int, int]:
         op = ReduceOp.parse(op)
+        if op is ReduceOp.PROD:
+            raise UsageError("PROD is an extension op (north_star): the reference's TCP peers do not implement it")
         if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1 or not buffer.is_contiguous() or not buffer.is_cuda:
             raise UsageError("buffer must be a one-dimensional contiguous CUDA tensor")
         if buffer.dtype not in DTYPE_CODE or (quantize and buffer.dtype != torch.float32):

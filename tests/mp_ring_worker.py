@@ -236,6 +236,19 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             check("qedge: schedule mismatch rejected", rejected)
             check("qedge: schedule mismatch intact", buf.cpu().numpy().tobytes() == inputs[eng.position].tobytes())
             eng.close()
+        if "ext" in scenarios:
+            # PROD extension (parity unpinned: oracle/ring.py's np.multiply fold)
+            multi = DeviceRing(device=dev, capacity_bytes=64 << 20, timeout_s=20.0, small_max_bytes=0)
+            for n in (1, 4099, 300_007):
+                g_ = np.random.default_rng(n)
+                inputs = [(1.0 + 0.05 * g_.normal(0, 1, n)).astype(np.float32) for _ in range(world)]
+                for eng, tag in ((ring, "small"), (multi, "multi-kernel")):
+                    for quant in (False, True):
+                        buf = torch.from_numpy(inputs[eng.position].copy()).to(dev)
+                        eng.run_all_reduce(buf, "prod", quantize=quant)
+                        want = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.PROD, quantize=quant)
+                        check(f"PROD {tag} n={n} q={quant}", buf.cpu().numpy().tobytes() == want.tobytes())
+            multi.close()
         if "large" in scenarios or "large_small" in scenarios:
             n = (1 << 24) + 3 if "large" in scenarios else (1 << 21) + 3
             for quant in (False, True):
@@ -367,5 +380,5 @@ if __name__ == "__main__":
     import torch.multiprocessing as mp
 
     world, port, outdir = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-    scenarios = sys.argv[4:] or ["golden", "faults", "registered", "qedge", "large"]
+    scenarios = sys.argv[4:] or ["golden", "faults", "registered", "qedge", "ext", "large"]
     mp.spawn(_entry, args=(world, port, outdir, scenarios), nprocs=world, join=True)

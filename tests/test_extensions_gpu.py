@@ -1,0 +1,67 @@
+"""North-star extensions absent from the reference (SURVEY §0, §8c "parity
+unpinned"): their oracle is this repo's own restatement in oracle/, defined
+the way the reference defines its ops (same fold order, same rounding rules),
+and the GPU paths must match it bit for bit.
+
+  PROD   np.multiply folded in the ring order (oracle/ring.py ReduceOp.PROD)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ring as oring
+from tests.gpu_util import bits, need_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    need_gpu()
+
+
+def _prod_inputs(w: int, n: int, dtype, seed: int) -> list[np.ndarray]:
+    # factors near 1 keep W-fold products finite; a few exact edge values
+    rng = np.random.default_rng(seed)
+    out = []
+    for p in range(w):
+        x = (1.0 + 0.05 * rng.normal(0, 1, n)).astype(dtype)
+        if n > 8:
+            x[:4] = np.array([0.0, -0.0, 2.0, -1.5], dtype=dtype)[: 4]
+        out.append(x)
+    return out
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("n", [0, 1, 7, 4099, 100_003])
+@pytest.mark.parametrize("dtype,quant", [(np.float32, False), (np.float64, False), (np.float32, True)])
+def test_prod_local_ring(w, n, dtype, quant):
+    from paper_2505_14065_b200 import LocalRing
+
+    host = _prod_inputs(w, n, dtype, 1000 * w + n)
+    want = oring.ring_allreduce_chunkwise(host, oring.ReduceOp.PROD, quantize=quant)
+    dev = [to_dev(h) for h in host]
+    res = LocalRing(w).run_op(dev, "prod", quantize=quant)
+    assert all(s == "ok" for s, _ in res)
+    for d in dev:
+        assert bits(d) == bits(want)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_prod_accumulate_kernel(dtype):
+    from paper_2505_14065_b200.collective import accumulate
+
+    rng = np.random.default_rng(5)
+    npd = np.float32 if dtype == torch.float32 else np.float64
+    a = rng.normal(0, 3, 100_001).astype(npd)
+    b = rng.normal(0, 3, 100_001).astype(npd)
+    a[:6] = [np.nan, 1.0, np.inf, 0.0, -0.0, 1e-40]
+    b[:6] = [2.0, np.nan, 0.0, np.inf, 5.0, 1e-5]
+    want = a.copy()
+    oring.accumulate(oring.ReduceOp.PROD, want, b)
+    da, db = to_dev(a), to_dev(b)
+    accumulate("prod", da, db)
+    assert bits(da) == bits(want)

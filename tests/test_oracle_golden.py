@@ -149,3 +149,17 @@ def test_outer_oracle_matches_reference_run(golden):
         g, vel = _outer_replay(int(n), oouter)
         assert osh.simplehash_c(g) == want["params"]
         assert osh.simplehash_c(vel) == want["velocity"]
+
+
+@pytest.mark.parametrize("w", [2, 3, 4, 8])
+@pytest.mark.parametrize("quant", [False, True])
+def test_prod_extension_closed_form_matches_ring(w, quant):
+    """The PROD extension (parity unpinned: no reference op) is defined as the
+    reference's ring with np.multiply; the chunk closed form agrees with the
+    full ring simulation, as it does for the reference's own ops."""
+    rng = np.random.default_rng(w)
+    bufs = [(1.0 + 0.05 * rng.normal(0, 1, 4099)).astype(np.float32) for _ in range(w)]
+    ring = oring.ring_allreduce([b.copy() for b in bufs], oring.ReduceOp.PROD, quantize=quant)
+    closed = oring.ring_allreduce_chunkwise(bufs, oring.ReduceOp.PROD, quantize=quant)
+    for out in ring:
+        assert out.tobytes() == closed.tobytes()

@@ -39,7 +39,7 @@ def _scenarios(world: int) -> list[str]:
     if n >= world:
         return []  # the worker's default: everything
     # oversubscribed: ranks time-slice one GPU, so keep the sizes small
-    return ["golden", "faults", "registered", "qedge", "large_small"]
+    return ["golden", "faults", "registered", "qedge", "ext", "large_small"]
 
 
 @pytest.mark.parametrize("world", _worlds())
