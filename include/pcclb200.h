@@ -156,6 +156,15 @@ PCCLB_API int pcclb_simplehash_update(uint64_t *d_state, const void *d_data, uin
 PCCLB_API int pcclb_simplehash_final(const uint64_t *d_state, uint64_t total_nbytes, uint64_t *d_out,
                            void *stream);
 
+/* CRC-32 digests (extension: the north_star's "simplehash/CRC32"; absent from
+ * the reference). zlib.crc32 of each device buffer -- reflected polynomial
+ * 0xEDB88320, init and final xor 0xFFFFFFFF -- written to d_out[i] (uint32).
+ * One launch for all entries (256 KiB segments per CTA, combined with
+ * GF(2) shifts). Parity is pinned by zlib itself. */
+PCCLB_API int pcclb_crc32_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, uint32_t count,
+                                uint32_t *d_out, void *stream);
+PCCLB_API int pcclb_crc32(const void *d_data, uint64_t nbytes, uint32_t *d_out, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* local ring: W logical peers whose buffers live on ONE GPU                 */
 /* (the reference's in-process RingSession, tests/ring_harness.py:24-105)    */

@@ -17,6 +17,6 @@ from .collective import (  # noqa: F401
     quantize_chunk,
 )
 from .ring import LocalRing  # noqa: F401
-from .sharedstate import SharedStateEntry, digest_entries, simplehash, simplehash_many  # noqa: F401
+from .sharedstate import SharedStateEntry, crc32, crc32_many, digest_entries, simplehash, simplehash_many  # noqa: F401
 
 __version__ = "0.1.0"

@@ -85,6 +85,8 @@ SIGNATURES = {
     "pcclb_dequant_accumulate_u8": (_I, [_P, _P, _U64, _P, _I, _P, _P]),
     "pcclb_simplehash": (_I, [_P, _U64, _P, _P]),
     "pcclb_simplehash_multi": (_I, [ctypes.POINTER(_P), ctypes.POINTER(_U64), _U32, _P, _P]),
+    "pcclb_crc32": (_I, [_P, _U64, _P, _P]),
+    "pcclb_crc32_multi": (_I, [ctypes.POINTER(_P), ctypes.POINTER(_U64), _U32, _P, _P]),
     "pcclb_simplehash_init": (_I, [_P, _P]),
     "pcclb_simplehash_update": (_I, [_P, _P, _U64, _P]),
     "pcclb_simplehash_final": (_I, [_P, _U64, _P, _P]),

@@ -80,6 +80,28 @@ def simplehash_many(tensors: list[torch.Tensor]) -> list[int]:
     return _to_u64(out)
 
 
+def crc32_many(tensors: list[torch.Tensor]) -> list[int]:
+    """zlib.crc32 of the raw bytes of CUDA tensors, one launch for all
+    (extension digest, csrc/crc.cu; parity pinned by zlib)."""
+    n = len(tensors)
+    if n == 0:
+        return []
+    ptrs = (ctypes.c_void_p * n)()
+    sizes = (ctypes.c_uint64 * n)()
+    for i, t in enumerate(tensors):
+        p, nb = _device_bytes(t)
+        ptrs[i] = p
+        sizes[i] = nb
+    out = torch.empty(n, dtype=torch.int32, device=tensors[0].device)
+    check(lib().pcclb_crc32_multi(ptrs, sizes, n, out.data_ptr(), _stream()), "crc32_multi")
+    return [int(x) & 0xFFFFFFFF for x in out.cpu().tolist()]
+
+
+def crc32(tensor: torch.Tensor) -> int:
+    """zlib.crc32 of a CUDA tensor's bytes."""
+    return crc32_many([tensor])[0]
+
+
 class StreamingHasher:
     """Hash a host byte stream on the GPU: pinned double-buffered staging,
     H2D copy of segment i+1 overlapped with hashing of segment i."""

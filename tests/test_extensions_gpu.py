@@ -65,3 +65,41 @@ def test_prod_accumulate_kernel(dtype):
     da, db = to_dev(a), to_dev(b)
     accumulate("prod", da, db)
     assert bits(da) == bits(want)
+
+
+# ---------------------------------------------------------------------------
+# CRC-32 (csrc/crc.cu): the checker is zlib.crc32 itself
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [0, 1, 3, 15, 16, 17, 1023, 1024, 1025, 262143, 262144, 262145,
+                               (1 << 20) + 7, (3 << 20) + 262144 * 2 + 5])
+def test_crc32_sizes(n):
+    import zlib
+
+    from paper_2505_14065_b200 import crc32
+
+    raw = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
+    assert crc32(to_dev(raw)) == zlib.crc32(raw.tobytes())
+
+
+@pytest.mark.parametrize("offset", [1, 2, 5, 8, 13])
+def test_crc32_misaligned(offset):
+    import zlib
+
+    from paper_2505_14065_b200 import crc32
+
+    raw = np.random.default_rng(offset).integers(0, 256, (1 << 20) + 99, dtype=np.uint8)
+    dev = to_dev(raw)
+    assert crc32(dev[offset:]) == zlib.crc32(raw[offset:].tobytes())
+
+
+def test_crc32_many_and_large():
+    """A multi-entry call (config-4-like mix) and a 1.05 GB entry."""
+    import zlib
+
+    from paper_2505_14065_b200 import crc32_many
+
+    rng = np.random.default_rng(3)
+    sizes = [int(x) for x in rng.integers(0, 3 << 20, 40)] + [0, 1, 1050673152]
+    host = [rng.integers(0, 256, s, dtype=np.uint8) for s in sizes]
+    got = crc32_many([to_dev(h) for h in host])
+    assert got == [zlib.crc32(h.tobytes()) for h in host]
