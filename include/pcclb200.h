@@ -55,6 +55,17 @@ enum { PCCLB_SUM = 1, PCCLB_AVG = 2, PCCLB_MAX = 3, PCCLB_MIN = 4 };
  * Not sent over the reference's TCP frames (off-box peers reject it). */
 enum { PCCLB_PROD = 5 };
 
+/* Quantization formats. PCCLB_Q_U8 is the reference's (collective.py:109-135:
+ * per-span min-max affine u8). The others are north_star extensions (parity
+ * unpinned; oracle/quant_ext.py defines them the same way):
+ *   U16:    scale = (max - min) / 65535 (1 if 0), q = u16(clip(rint((x - min) / scale)))
+ *   U8_ZP / U16_ZP: min/max widened to include 0, scale = (max - min) / L (1 if 0),
+ *           zp = clip(rint(-min / scale), 0, L),
+ *           q = clip(rint(x / scale) + zp, 0, L), D(q) = (q - zp) * scale
+ * (L = 255 / 65535; NaN -> code 0; IEEE RN, no FMA). Single-GPU seams and the
+ * local ring take every format; the NVLink and TCP engines take U8 only. */
+enum { PCCLB_Q_U8 = 1, PCCLB_Q_U16 = 2, PCCLB_Q_U8_ZP = 3, PCCLB_Q_U16_ZP = 4 };
+
 /* Span range accumulator for quantization (collective.py:117-121).
  * Order-preserving u32 keys so device atomics can reduce min/max; all-zero
  * bytes is the empty range (pcclb_range_reset is a memset). kmin_inv holds
@@ -126,6 +137,15 @@ PCCLB_API int pcclb_dequantize_u8(float *out, const uint8_t *codes, uint64_t n, 
 PCCLB_API int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint64_t n,
                                 const pcclb_qmeta *d_meta, int op, pcclb_range *d_next_range,
                                 void *stream);
+/* The three seams for any quantization format (PCCLB_Q_*; codes are u8 or
+ * u16 per format; for the _ZP formats d_meta->min_val holds the zero point).
+ * PCCLB_Q_U8 forwards to the _u8 functions above. */
+PCCLB_API int pcclb_quantize_ex(const float *x, uint64_t n, const pcclb_range *d_range, void *codes,
+                                pcclb_qmeta *d_meta, float *adopt_out, uint32_t avg_div, int qformat, void *stream);
+PCCLB_API int pcclb_dequantize_ex(float *out, const void *codes, uint64_t n, const pcclb_qmeta *d_meta,
+                                  uint32_t avg_div, int qformat, void *stream);
+PCCLB_API int pcclb_dequant_accumulate_ex(float *acc, const void *codes, uint64_t n, const pcclb_qmeta *d_meta,
+                                          int op, pcclb_range *d_next_range, int qformat, void *stream);
 
 /* Outer-optimizer steps of the DiLoCo loops around the all-reduce, with the
  * reference's rounding sequence (algos.py:79-105, :236-239):
@@ -178,6 +198,9 @@ PCCLB_API int pcclb_crc32(const void *d_data, uint64_t nbytes, uint32_t *d_out, 
 PCCLB_API uint64_t pcclb_local_scratch_bytes(uint32_t world);
 PCCLB_API int pcclb_local_allreduce(void *const *h_bufs, uint32_t world, uint64_t n, int dtype, int op,
                           int quantize, void *d_scratch, void *d_backup, void *stream);
+/* Same with a quantization format (0 = none, PCCLB_Q_*). */
+PCCLB_API int pcclb_local_allreduce_ex(void *const *h_bufs, uint32_t w, uint64_t n, int dtype, int op,
+                                       int qformat, void *d_scratch, void *d_backup, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* intra-box ring over NVLink: one process per GPU                           */

@@ -83,6 +83,9 @@ SIGNATURES = {
     "pcclb_quantize_u8": (_I, [_P, _U64, _P, _P, _P, _P, _U32, _P]),
     "pcclb_dequantize_u8": (_I, [_P, _P, _U64, _P, _U32, _P]),
     "pcclb_dequant_accumulate_u8": (_I, [_P, _P, _U64, _P, _I, _P, _P]),
+    "pcclb_quantize_ex": (_I, [_P, _U64, _P, _P, _P, _P, _U32, _I, _P]),
+    "pcclb_dequantize_ex": (_I, [_P, _P, _U64, _P, _U32, _I, _P]),
+    "pcclb_dequant_accumulate_ex": (_I, [_P, _P, _U64, _P, _I, _P, _I, _P]),
     "pcclb_simplehash": (_I, [_P, _U64, _P, _P]),
     "pcclb_simplehash_multi": (_I, [ctypes.POINTER(_P), ctypes.POINTER(_U64), _U32, _P, _P]),
     "pcclb_crc32": (_I, [_P, _U64, _P, _P]),
@@ -95,6 +98,7 @@ SIGNATURES = {
     "pcclb_outer_nesterov_f32": (_I, [_P, _P, _P, _U64, ctypes.c_float, ctypes.c_float, _P]),
     "pcclb_local_scratch_bytes": (_U64, [_U32]),
     "pcclb_local_allreduce": (_I, [ctypes.POINTER(_P), _U32, _U64, _I, _I, _I, _P, _P, _P]),
+    "pcclb_local_allreduce_ex": (_I, [ctypes.POINTER(_P), _U32, _U64, _I, _I, _I, _P, _P, _P]),
     "pcclb_ring_create": (_I, [_I, _U32, _U32, _U64, ctypes.POINTER(_P)]),
     "pcclb_ring_export": (_I, [_P, _P]),
     "pcclb_ring_import": (_I, [_P, _U32, _P]),

@@ -73,6 +73,23 @@ class ReduceOp(Enum):
 _OP_CODE = {ReduceOp.SUM: 1, ReduceOp.AVG: 2, ReduceOp.MAX: 3, ReduceOp.MIN: 4, ReduceOp.PROD: 5}
 _CODE_OP = {v: k for k, v in _OP_CODE.items()}
 
+# quantization formats (pcclb200.h PCCLB_Q_*): "u8" is the reference's
+# min-max u8 (collective.py:109-135); the others are extensions (parity
+# unpinned, oracle/quant_ext.py) that the single-GPU paths accept
+QFORMATS = {"u8": 1, "u16": 2, "u8_zp": 3, "u16_zp": 4}
+
+
+def qformat_code(quantize) -> int:
+    """0 for no quantization, else the PCCLB_Q_* code of `quantize` (a bool --
+    True is the reference's u8 -- or a format name)."""
+    if quantize is None or quantize is False:
+        return 0
+    if quantize is True:
+        return QFORMATS["u8"]
+    if isinstance(quantize, str) and quantize in QFORMATS:
+        return QFORMATS[quantize]
+    raise UsageError(f"unknown quantization format {quantize!r} (one of {sorted(QFORMATS)})")
+
 DTYPE_CODE = {torch.float32: F32, torch.float64: F64}
 
 

@@ -11,6 +11,8 @@
 // sized to a multiple of the SM count, arithmetic from numerics.cuh.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "elementwise.cuh"
 #include "numerics.cuh"
@@ -157,6 +159,73 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (next) range_block_commit(f.r, next);
 }
 
+// ---------------------------------------------------------------------------
+// quantization formats beyond u8 min-max (extensions, pcclb200.h PCCLB_Q_*):
+// grid-stride kernels over the format's code type
+// ---------------------------------------------------------------------------
+template <int QF>
+__global__ void __launch_bounds__(kThreads)
+    quantize_q_kernel(const float *x, uint64_t n, const pcclb_range *range, void *codes_v, pcclb_qmeta *meta,
+                      float *adopt, uint32_t avg_div) {
+  using C = typename QFmt<QF>::Code;
+  C *codes = static_cast<C *>(codes_v);
+  const QParams qp = qparams_q<QF>(*range);
+  if (meta && blockIdx.x == 0 && threadIdx.x == 0) {
+    meta->min_val = qp.mn;  // the zero point for the _ZP formats
+    meta->scale = qp.scale;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = quantq<QF>(x[i], qp);
+    codes[i] = (C)q;
+    if (adopt) {
+      const float d = dequantq<QF>(q, qp);
+      adopt[i] = avg_div > 1 ? div_world(d, (float)avg_div) : d;
+    }
+  }
+}
+
+template <int QF>
+__global__ void __launch_bounds__(kThreads)
+    dequantize_q_kernel(float *out, const void *codes_v, uint64_t n, const pcclb_qmeta *meta, uint32_t avg_div) {
+  using C = typename QFmt<QF>::Code;
+  const C *codes = static_cast<const C *>(codes_v);
+  const QParams qp{meta->min_val, meta->scale, 0.0f};
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float d = dequantq<QF>(codes[i], qp);
+    out[i] = avg_div > 1 ? div_world(d, (float)avg_div) : d;
+  }
+}
+
+template <int QF, int OP>
+__global__ void __launch_bounds__(kThreads)
+    dequant_acc_q_kernel(float *acc, const void *codes_v, uint64_t n, const pcclb_qmeta *meta, pcclb_range *next) {
+  using C = typename QFmt<QF>::Code;
+  const C *codes = static_cast<const C *>(codes_v);
+  const QParams qp{meta->min_val, meta->scale, 0.0f};
+  RangeAcc r;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = reduce_op<OP>(acc[i], dequantq<QF>(codes[i], qp));
+    acc[i] = v;
+    if (next) r.add(v);
+  }
+  if (next) range_block_commit(r, next);
+}
+
+template <class F>
+static int with_qformat(int qformat, F f) {
+  switch (qformat) {
+    case PCCLB_Q_U8:
+      return f(std::integral_constant<int, PCCLB_Q_U8>());
+    case PCCLB_Q_U16:
+      return f(std::integral_constant<int, PCCLB_Q_U16>());
+    case PCCLB_Q_U8_ZP:
+      return f(std::integral_constant<int, PCCLB_Q_U8_ZP>());
+    case PCCLB_Q_U16_ZP:
+      return f(std::integral_constant<int, PCCLB_Q_U16_ZP>());
+  }
+  return PCCLB_EINVAL;
+}
+
 // float/code pointer pair vectorizable with the same peel?
 static bool fc_vec_ok(const float *x, const uint8_t *codes, uint64_t *head) {
   uint64_t h = peel16<float>(x);
@@ -265,6 +334,65 @@ int pcclb_dequant_accumulate_u8(float *acc, const uint8_t *codes, uint64_t n,
 #undef PCCLB_DQA
   PCCLB_LAUNCH_CHECK();
   return PCCLB_OK;
+}
+
+int pcclb_quantize_ex(const float *x, uint64_t n, const pcclb_range *d_range, void *codes, pcclb_qmeta *d_meta,
+                      float *adopt_out, uint32_t avg_div, int qformat, void *stream) {
+  if (qformat == PCCLB_Q_U8)
+    return pcclb_quantize_u8(x, n, d_range, static_cast<uint8_t *>(codes), d_meta, adopt_out, avg_div, stream);
+  if (!d_range || (n && (!x || !codes)) || avg_div < 1) return PCCLB_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for(n ? n : 1, (uint64_t)kThreads * 8);
+  return with_qformat(qformat, [&](auto qf) -> int {
+    quantize_q_kernel<decltype(qf)::value><<<grid, kThreads, 0, s>>>(x, n, d_range, codes, d_meta, adopt_out, avg_div);
+    PCCLB_LAUNCH_CHECK();
+    return PCCLB_OK;
+  });
+}
+
+int pcclb_dequantize_ex(float *out, const void *codes, uint64_t n, const pcclb_qmeta *d_meta, uint32_t avg_div,
+                        int qformat, void *stream) {
+  if (qformat == PCCLB_Q_U8)
+    return pcclb_dequantize_u8(out, static_cast<const uint8_t *>(codes), n, d_meta, avg_div, stream);
+  if (!d_meta || (n && (!out || !codes)) || avg_div < 1) return PCCLB_EINVAL;
+  if (n == 0) return PCCLB_OK;
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for(n, (uint64_t)kThreads * 8);
+  return with_qformat(qformat, [&](auto qf) -> int {
+    dequantize_q_kernel<decltype(qf)::value><<<grid, kThreads, 0, s>>>(out, codes, n, d_meta, avg_div);
+    PCCLB_LAUNCH_CHECK();
+    return PCCLB_OK;
+  });
+}
+
+int pcclb_dequant_accumulate_ex(float *acc, const void *codes, uint64_t n, const pcclb_qmeta *d_meta, int op,
+                                pcclb_range *d_next_range, int qformat, void *stream) {
+  if (qformat == PCCLB_Q_U8)
+    return pcclb_dequant_accumulate_u8(acc, static_cast<const uint8_t *>(codes), n, d_meta, op, d_next_range,
+                                       stream);
+  if (!d_meta || !valid_op(op) || (n && (!acc || !codes))) return PCCLB_EINVAL;
+  if (n == 0) return PCCLB_OK;
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for(n, (uint64_t)kThreads * 8);
+  return with_qformat(qformat, [&](auto qf) -> int {
+    constexpr int QF = decltype(qf)::value;
+    switch (op) {
+      case PCCLB_MAX:
+        dequant_acc_q_kernel<QF, PCCLB_MAX><<<grid, kThreads, 0, s>>>(acc, codes, n, d_meta, d_next_range);
+        break;
+      case PCCLB_MIN:
+        dequant_acc_q_kernel<QF, PCCLB_MIN><<<grid, kThreads, 0, s>>>(acc, codes, n, d_meta, d_next_range);
+        break;
+      case PCCLB_PROD:
+        dequant_acc_q_kernel<QF, PCCLB_PROD><<<grid, kThreads, 0, s>>>(acc, codes, n, d_meta, d_next_range);
+        break;
+      default:
+        dequant_acc_q_kernel<QF, PCCLB_SUM><<<grid, kThreads, 0, s>>>(acc, codes, n, d_meta, d_next_range);
+        break;
+    }
+    PCCLB_LAUNCH_CHECK();
+    return PCCLB_OK;
+  });
 }
 
 }  // extern "C"

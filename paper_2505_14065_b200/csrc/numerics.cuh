@@ -17,6 +17,8 @@
 
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "pcclb200.h"
 
 namespace pcclb {
@@ -203,6 +205,88 @@ __device__ __forceinline__ uint32_t quant1_fast(float x, float mn, float scale, 
     return (uint32_t)q;
   }
   return quant1_exact(x, mn, scale);
+}
+
+// ---------------------------------------------------------------------------
+// quantization formats beyond the reference's u8 min-max (extensions, see
+// pcclb200.h PCCLB_Q_*): qparams_q / quantq / dequantq. For PCCLB_Q_U8 they
+// are exactly qparams_from_range / quant1_fast / dequant1.
+// ---------------------------------------------------------------------------
+template <int QF>
+struct QFmt {
+  static constexpr float kLevels = (QF == PCCLB_Q_U16 || QF == PCCLB_Q_U16_ZP) ? 65535.0f : 255.0f;
+  static constexpr bool kZp = QF == PCCLB_Q_U8_ZP || QF == PCCLB_Q_U16_ZP;
+  using Code = typename std::conditional<(QF == PCCLB_Q_U16 || QF == PCCLB_Q_U16_ZP), uint16_t, uint8_t>::type;
+};
+
+// round t (finite or not) to an integer code in [0, L]; NaN -> 0
+template <int QF>
+__device__ __forceinline__ uint32_t clip_code(float t) {
+  if (is_nan(t)) return 0u;
+  return (uint32_t)fminf(fmaxf(t, 0.0f), QFmt<QF>::kLevels);
+}
+
+// QParams.mn holds the minimum (min-max) or the zero point (as a float)
+template <int QF>
+__device__ __forceinline__ QParams qparams_q(const pcclb_range &r) {
+  if constexpr (QF == PCCLB_Q_U8) {
+    return qparams_from_range(r);
+  } else {
+    QParams q;
+    if (!r.seen) {
+      q.mn = 0.0f;
+      q.scale = 1.0f;
+      q.inv = 1.0f;
+      return q;
+    }
+    float mn = fkey_decode(~r.kmin_inv), mx = fkey_decode(r.kmax);
+    if constexpr (QFmt<QF>::kZp) {
+      // the range is widened to include 0, which the zero point then encodes
+      // exactly (asymmetric affine quantization, like PyTorch's MinMaxObserver)
+      mn = fminf(mn, 0.0f);
+      mx = fmaxf(mx, 0.0f);
+    }
+    float s = x86_div(x86_sub(mx, mn), QFmt<QF>::kLevels);
+    if (s == 0.0f) s = 1.0f;
+    q.scale = s;
+    q.inv = __fdiv_rn(1.0f, s);
+    if constexpr (QFmt<QF>::kZp) q.mn = (float)clip_code<QF>(rintf(__fdiv_rn(-mn, s)));
+    else q.mn = mn;
+    return q;
+  }
+}
+
+template <int QF>
+__device__ __noinline__ uint32_t quantq_exact(float x, float mn, float scale) {
+  if constexpr (QFmt<QF>::kZp) return clip_code<QF>(__fadd_rn(rintf(__fdiv_rn(x, scale)), mn));
+  else return clip_code<QF>(rintf(__fdiv_rn(__fsub_rn(x, mn), scale)));
+}
+
+// exactness-guarded reciprocal like quant1_fast: the product is used unless
+// it lies within ~2^-20 (relative) of a half-integer
+template <int QF>
+__device__ __forceinline__ uint32_t quantq(float x, const QParams &qp) {
+  if constexpr (QF == PCCLB_Q_U8) {
+    return quant1_fast(x, qp.mn, qp.scale, qp.inv);
+  } else {
+    const float d = QFmt<QF>::kZp ? x : __fsub_rn(x, qp.mn);
+    const float t = __fmul_rn(d, qp.inv);
+    const float fl = floorf(t);
+    const float h = __fsub_rn(t, fl);
+    const float m = fabsf(__fsub_rn(h, 0.5f));
+    if (__builtin_expect(m > __fmul_rn(fabsf(t), 1e-6f) + 1e-30f && fabsf(t) < 8388608.0f, 1)) {
+      float q = (h > 0.5f) ? __fadd_rn(fl, 1.0f) : fl;
+      if constexpr (QFmt<QF>::kZp) q = __fadd_rn(q, qp.mn);
+      return clip_code<QF>(q);
+    }
+    return quantq_exact<QF>(x, qp.mn, qp.scale);
+  }
+}
+
+template <int QF>
+__device__ __forceinline__ float dequantq(uint32_t q, const QParams &qp) {
+  if constexpr (QFmt<QF>::kZp) return x86_mul(__fsub_rn((float)q, qp.mn), qp.scale);
+  else return x86_add(x86_mul((float)q, qp.scale), qp.mn);
 }
 
 // x = f32(q) * scale (RN) + min (RN), x86 NaN rules

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kLocalThreads, 4)
 }
 
 // hop k >= 1: x_{c+k} <- x_{c+k} (+) D(Q(acc_{k-1})), range -> ranges[c*w + k]
-template <int OP>
+template <int OP, int QF>
 __global__ void __launch_bounds__(kLocalThreads, 4)
     local_q_hop_kernel(const __grid_constant__ LocalBufs<float> P, pcclb_range *ranges, uint32_t k) {
   const uint32_t c = blockIdx.y;
@@ -182,12 +182,12 @@ __global__ void __launch_bounds__(kLocalThreads, 4)
   if (len == 0) return;
   const float *prev = P.b[(c + k - 1) % w] + lo;
   float *cur = P.b[(c + k) % w] + lo;
-  const QParams qp = qparams_from_range(ranges[(uint64_t)c * w + k - 1]);
+  const QParams qp = qparams_q<QF>(ranges[(uint64_t)c * w + k - 1]);
   RangeAcc acc;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   auto one = [&](uint64_t i) {
-    float d = dequant1(quant1_fast(prev[i], qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
+    float d = dequantq<QF>(quantq<QF>(prev[i], qp), qp);
     float v = reduce_op<OP>(cur[i], d);
     cur[i] = v;
     acc.add(v);
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kLocalThreads, 4)
   auto apply = [&](uint64_t i, const Pack16<float> &pv, Pack16<float> cv) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float d = dequant1(quant1_fast(pv.e[e], qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
+      float d = dequantq<QF>(quantq<QF>(pv.e[e], qp), qp);
       cv.e[e] = reduce_op<OP>(cv.e[e], d);
       acc.add(cv.e[e]);
     }
@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kLocalThreads, 4)
 }
 
 // owner adoption + AVG + gather: every buffer's chunk c <- D(Q(acc_{W-1})) [/W]
+template <int QF>
 __global__ void __launch_bounds__(kLocalThreads, 4)
     local_q_final_kernel(const __grid_constant__ LocalBufs<float> P, const pcclb_range *ranges) {
   const uint32_t c = blockIdx.y;
@@ -236,10 +237,10 @@ __global__ void __launch_bounds__(kLocalThreads, 4)
   if (len == 0) return;
   const uint32_t owner = (c + w - 1) % w;
   const float *acc = P.b[owner] + lo;
-  const QParams qp = qparams_from_range(ranges[(uint64_t)c * w + w - 1]);
+  const QParams qp = qparams_q<QF>(ranges[(uint64_t)c * w + w - 1]);
   const float avg = (float)P.avg;
   auto val = [&](float x) {
-    float d = dequant1(quant1_fast(x, qp.mn, qp.scale, qp.inv), qp.mn, qp.scale);
+    float d = dequantq<QF>(quantq<QF>(x, qp), qp);
     return P.avg ? div_world(d, avg) : d;
   };
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,6 +298,32 @@ static int local_plain(const LocalBufs<T> &P, int op, bool vec, dim3 grid, cudaS
   return PCCLB_OK;
 }
 
+
+// hops 1..W-1 and the final adoption+gather for quantization format QF
+template <int QF>
+int local_q_hops(const LocalBufs<float> &P, pcclb_range *ranges, int op, dim3 grid, cudaStream_t s) {
+  for (uint32_t k = 1; k < P.w; ++k) {
+    switch (op) {
+      case PCCLB_MAX:
+        local_q_hop_kernel<PCCLB_MAX, QF><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
+        break;
+      case PCCLB_MIN:
+        local_q_hop_kernel<PCCLB_MIN, QF><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
+        break;
+      case PCCLB_PROD:
+        local_q_hop_kernel<PCCLB_PROD, QF><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
+        break;
+      default:
+        local_q_hop_kernel<PCCLB_SUM, QF><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
+        break;
+    }
+    PCCLB_LAUNCH_CHECK();
+  }
+  local_q_final_kernel<QF><<<grid, kLocalThreads, 0, s>>>(P, ranges);
+  PCCLB_LAUNCH_CHECK();
+  return PCCLB_OK;
+}
+
 }  // namespace pcclb
 
 using namespace pcclb;
@@ -309,7 +336,15 @@ uint64_t pcclb_local_scratch_bytes(uint32_t world) {
 
 int pcclb_local_allreduce(void *const *h_bufs, uint32_t w, uint64_t n, int dtype, int op,
                           int quantize, void *d_scratch, void *d_backup, void *stream) {
-  if (!h_bufs || w < 1 || w > (uint32_t)kMaxWorld || !valid_dtype(dtype) || !valid_op(op))
+  return pcclb_local_allreduce_ex(h_bufs, w, n, dtype, op, quantize ? PCCLB_Q_U8 : 0, d_scratch, d_backup,
+                                  stream);
+}
+
+int pcclb_local_allreduce_ex(void *const *h_bufs, uint32_t w, uint64_t n, int dtype, int op, int qformat,
+                             void *d_scratch, void *d_backup, void *stream) {
+  const int quantize = qformat != 0;
+  if (!h_bufs || w < 1 || w > (uint32_t)kMaxWorld || !valid_dtype(dtype) || !valid_op(op) || qformat < 0 ||
+      qformat > PCCLB_Q_U16_ZP)
     return PCCLB_EINVAL;
   if (quantize && dtype != PCCLB_F32) return PCCLB_EINVAL;  // client.py:818-819
   for (uint32_t i = 0; i < w; ++i)
@@ -352,25 +387,22 @@ int pcclb_local_allreduce(void *const *h_bufs, uint32_t w, uint64_t n, int dtype
   PCCLB_CUDA(cudaMemsetAsync(ranges, 0, pcclb_local_scratch_bytes(w), s));
   local_q_range0_kernel<<<grid, kLocalThreads, 0, s>>>(P, ranges);
   PCCLB_LAUNCH_CHECK();
-  for (uint32_t k = 1; k < w; ++k) {
-    switch (op) {
-      case PCCLB_MAX:
-        local_q_hop_kernel<PCCLB_MAX><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
-        break;
-      case PCCLB_MIN:
-        local_q_hop_kernel<PCCLB_MIN><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
-        break;
-      case PCCLB_PROD:
-        local_q_hop_kernel<PCCLB_PROD><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
-        break;
-      default:
-        local_q_hop_kernel<PCCLB_SUM><<<grid, kLocalThreads, 0, s>>>(P, ranges, k);
-        break;
-    }
-    PCCLB_LAUNCH_CHECK();
+  int rcq = PCCLB_OK;
+  switch (qformat) {
+    case PCCLB_Q_U16:
+      rcq = local_q_hops<PCCLB_Q_U16>(P, ranges, op, grid, s);
+      break;
+    case PCCLB_Q_U8_ZP:
+      rcq = local_q_hops<PCCLB_Q_U8_ZP>(P, ranges, op, grid, s);
+      break;
+    case PCCLB_Q_U16_ZP:
+      rcq = local_q_hops<PCCLB_Q_U16_ZP>(P, ranges, op, grid, s);
+      break;
+    default:
+      rcq = local_q_hops<PCCLB_Q_U8>(P, ranges, op, grid, s);
+      break;
   }
-  local_q_final_kernel<<<grid, kLocalThreads, 0, s>>>(P, ranges);
-  PCCLB_LAUNCH_CHECK();
+  if (rcq) return rcq;
   // every quantized span must have been finite (collective.py:117-118)
   std::vector<pcclb_range> host(w * w);
   PCCLB_CUDA(cudaMemcpyAsync(host.data(), ranges, pcclb_local_scratch_bytes(w),

@@ -17,7 +17,7 @@ import torch
 
 from . import _native
 from ._native import check, lib
-from .collective import DTYPE_CODE, CollectiveAborted, ReduceOp, UsageError
+from .collective import DTYPE_CODE, CollectiveAborted, ReduceOp, UsageError, qformat_code
 
 
 class LocalRing:
@@ -42,10 +42,12 @@ class LocalRing:
             self._backup = torch.empty(need, dtype=dtype, device=self.device)  # pool: reused
         return self._backup
 
-    def launch(self, buffers: list[torch.Tensor], op, quantize: bool = False, stream=None) -> int:
+    def launch(self, buffers: list[torch.Tensor], op, quantize=False, stream=None) -> int:
         """Enqueue the op on `stream` (plain ops never block the host);
-        returns the raw status."""
+        returns the raw status. `quantize`: False, True (the reference's u8
+        min-max) or an extension format name ("u16", "u8_zp", "u16_zp")."""
         op = ReduceOp.parse(op)
+        qf = qformat_code(quantize)
         if len(buffers) != self.world:
             raise UsageError(f"expected {self.world} buffers")
         b0 = buffers[0]
@@ -62,11 +64,11 @@ class LocalRing:
         ptrs = (ctypes.c_void_p * self.world)(*[b.data_ptr() for b in buffers])
         backup = self._backup_buf(n, b0.dtype).data_ptr() if (self.backup_enabled and quantize) else None
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        return lib().pcclb_local_allreduce(
-            ptrs, self.world, n, DTYPE_CODE[b0.dtype], op.code, int(quantize), self.scratch.data_ptr(), backup, s
+        return lib().pcclb_local_allreduce_ex(
+            ptrs, self.world, n, DTYPE_CODE[b0.dtype], op.code, qf, self.scratch.data_ptr(), backup, s
         )
 
-    def run_op(self, buffers: list[torch.Tensor], op, quantize: bool = False) -> list[tuple[str, object]]:
+    def run_op(self, buffers: list[torch.Tensor], op, quantize=False) -> list[tuple[str, object]]:
         """Run one attempt on all ranks; per-rank (status, extra) like RingSession.run_op."""
         rc = self.launch(buffers, op, quantize)
         if rc == _native.PCCLB_OK:

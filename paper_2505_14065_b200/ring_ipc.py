@@ -216,6 +216,8 @@ class DeviceRing:
             raise UsageError(f"unsupported dtype {buffer.dtype}")
         if quantize and buffer.dtype != torch.float32:
             raise UsageError("quantization requires float32 buffers")
+        if quantize not in (False, True, None, "u8"):
+            raise UsageError(f"the NVLink engine quantizes u8 min-max only (the reference's format), not {quantize!r}")
         return op
 
     def all_reduce_async(self, buffer: torch.Tensor, op=ReduceOp.SUM, quantize: bool = False,

@@ -173,6 +173,8 @@ class TcpRingEngine:
         op = ReduceOp.parse(op)
         if op is ReduceOp.PROD:
             raise UsageError("PROD is an extension op (north_star): the reference's TCP peers do not implement it")
+        if quantize not in (False, True, None, "u8"):
+            raise UsageError(f"the TCP frames carry u8 min-max codes only (wire.py QuantMeta), not {quantize!r}")
         if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1 or not buffer.is_contiguous() or not buffer.is_cuda:
             raise UsageError("buffer must be a one-dimensional contiguous CUDA tensor")
         if buffer.dtype not in DTYPE_CODE or (quantize and buffer.dtype != torch.float32):

@@ -103,3 +103,78 @@ def test_crc32_many_and_large():
     host = [rng.integers(0, 256, s, dtype=np.uint8) for s in sizes]
     got = crc32_many([to_dev(h) for h in host])
     assert got == [zlib.crc32(h.tobytes()) for h in host]
+
+
+# ---------------------------------------------------------------------------
+# u16 and zero-point quantization (oracle/quant_ext.py)
+# ---------------------------------------------------------------------------
+FMTS = ["u16", "u8_zp", "u16_zp"]
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("w", [2, 3, 5, 8])
+@pytest.mark.parametrize("n", [1, 7, 4099, 100_003])
+@pytest.mark.parametrize("op", ["sum", "avg", "max", "prod"])
+def test_qformat_local_ring(fmt, w, n, op):
+    from oracle import quant_ext as oq
+    from paper_2505_14065_b200 import LocalRing
+
+    rng = np.random.default_rng(w * 100_000 + n)
+    if op == "prod":
+        host = [(1.0 + 0.05 * rng.normal(0, 1, n)).astype(np.float32) for _ in range(w)]
+    else:
+        host = [rng.normal(0.3 if fmt.endswith("zp") else 0, 1, n).astype(np.float32) for _ in range(w)]
+    want = oq.ring_allreduce_chunkwise_ex(host, oring.ReduceOp[op.upper()], fmt)
+    dev = [to_dev(h) for h in host]
+    res = LocalRing(w).run_op(dev, op, quantize=fmt)
+    assert all(s == "ok" for s, _ in res)
+    for d in dev:
+        assert bits(d) == bits(want)
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_qformat_kernel_seams(fmt):
+    """quantize_ex / dequantize_ex / dequant_accumulate_ex codes and values."""
+    import ctypes
+
+    from oracle import quant_ext as oq
+    from paper_2505_14065_b200 import _native
+    from paper_2505_14065_b200.collective import QFORMATS
+
+    L = _native.lib()
+    qf = QFORMATS[fmt]
+    rng = np.random.default_rng(11)
+    x = rng.normal(0.5, 2, 300_007).astype(np.float32)
+    x[:5] = [0.0, -0.0, 1e-30, -3.5, 7.25]
+    codes_want, p0, scale = oq.quantize_ex(x, fmt)
+    dx = to_dev(x)
+    rng_buf = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    meta = torch.zeros(2, dtype=torch.float32, device="cuda")
+    codes = torch.zeros(x.size, dtype=torch.int16 if "16" in fmt else torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.pcclb_range_reset(rng_buf.data_ptr(), 1, s) == 0
+    assert L.pcclb_range_f32(dx.data_ptr(), x.size, rng_buf.data_ptr(), s) == 0
+    assert L.pcclb_quantize_ex(dx.data_ptr(), x.size, rng_buf.data_ptr(), codes.data_ptr(), meta.data_ptr(),
+                               None, 1, qf, s) == 0
+    got_codes = codes.cpu().numpy().view(codes_want.dtype)
+    assert got_codes.tobytes() == codes_want.tobytes()
+    assert meta.cpu().numpy().tobytes() == np.array([p0, scale], np.float32).tobytes()
+    out = torch.empty_like(dx)
+    assert L.pcclb_dequantize_ex(out.data_ptr(), codes.data_ptr(), x.size, meta.data_ptr(), 1, qf, s) == 0
+    assert bits(out) == bits(oq.dequantize_ex(codes_want, p0, scale, fmt))
+    acc = to_dev(x[::-1].copy())
+    assert L.pcclb_dequant_accumulate_ex(acc.data_ptr(), codes.data_ptr(), x.size, meta.data_ptr(), 1, None,
+                                         qf, s) == 0
+    want = x[::-1].copy()
+    oring.accumulate(oring.ReduceOp.SUM, want, oq.dequantize_ex(codes_want, p0, scale, fmt))
+    assert bits(acc) == bits(want)
+    del ctypes
+
+
+def test_qformat_rejected_by_nvlink_and_tcp_engines():
+    from paper_2505_14065_b200.collective import UsageError, qformat_code
+
+    assert qformat_code(True) == 1 and qformat_code(False) == 0 and qformat_code("u16_zp") == 4
+    with pytest.raises(UsageError):
+        qformat_code("fp8")
+    del UsageError
