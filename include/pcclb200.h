@@ -48,6 +48,11 @@ typedef enum {
 
 /* wire.py:130-138 DType codes (only the collective dtypes) */
 enum { PCCLB_F32 = 1, PCCLB_F64 = 2 };
+/* Extension dtype (north_star; the reference reduces f32/f64 only, wire.py
+ * DType 1/2, so parity is unpinned, oracle/bf16.py): every fold step computes
+ * in f32 and rounds to bf16 (RNE). Plain ops only (quantization needs f32);
+ * not sent over the reference's TCP frames. */
+enum { PCCLB_BF16 = 3 };
 /* wire.py:141-145 ReduceOpCode; collective.py:43-71 ReduceOp/_ACCUMULATE */
 enum { PCCLB_SUM = 1, PCCLB_AVG = 2, PCCLB_MAX = 3, PCCLB_MIN = 4 };
 /* Extension (north_star; absent from the reference, wire.py:141-145, so its

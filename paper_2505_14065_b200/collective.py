@@ -90,7 +90,9 @@ def qformat_code(quantize) -> int:
         return QFORMATS[quantize]
     raise UsageError(f"unknown quantization format {quantize!r} (one of {sorted(QFORMATS)})")
 
-DTYPE_CODE = {torch.float32: F32, torch.float64: F64}
+# torch.bfloat16 (code 3) is an extension (pcclb200.h PCCLB_BF16): plain ops
+# on the single-GPU and NVLink paths; the reference's wire has f32/f64 only
+DTYPE_CODE = {torch.float32: F32, torch.float64: F64, torch.bfloat16: 3}
 
 
 def compute_chunk_boundaries(n_elements: int, world_size: int) -> list[tuple[int, int]]:
@@ -106,7 +108,7 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def _check_buffer(t: torch.Tensor, what: str, dtypes=(torch.float32, torch.float64)) -> None:
+def _check_buffer(t: torch.Tensor, what: str, dtypes=(torch.float32, torch.float64, torch.bfloat16)) -> None:
     if not isinstance(t, torch.Tensor):
         raise UsageError(f"{what} must be a torch.Tensor")
     if not t.is_cuda:

@@ -160,7 +160,7 @@ class Communicator:
         op = ReduceOp.parse(op)
         if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1:
             raise UsageError("buffer must be a one-dimensional tensor")
-        if buffer.dtype not in (torch.float32, torch.float64):
+        if buffer.dtype not in (torch.float32, torch.float64, torch.bfloat16):
             raise UsageError(f"unsupported dtype {buffer.dtype}")
         if not buffer.is_contiguous() or not buffer.is_cuda:
             raise UsageError("buffer must be a contiguous CUDA tensor")

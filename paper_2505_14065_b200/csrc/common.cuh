@@ -40,8 +40,8 @@ inline unsigned grid_for(uint64_t work, uint64_t per_cta, int ctas_per_sm = 8) {
   return (unsigned)need;
 }
 
-inline bool valid_dtype(int dt) { return dt == PCCLB_F32 || dt == PCCLB_F64; }
+inline bool valid_dtype(int dt) { return dt == PCCLB_F32 || dt == PCCLB_F64 || dt == PCCLB_BF16; }
 inline bool valid_op(int op) { return op >= PCCLB_SUM && op <= PCCLB_PROD; }
-inline size_t dtype_size(int dt) { return dt == PCCLB_F64 ? 8 : 4; }
+inline size_t dtype_size(int dt) { return dt == PCCLB_F64 ? 8 : dt == PCCLB_BF16 ? 2 : 4; }
 
 }  // namespace pcclb

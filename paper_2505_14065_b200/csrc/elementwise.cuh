@@ -11,6 +11,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <string.h>
 
 namespace pcclb {
 
@@ -43,6 +44,14 @@ __device__ __forceinline__ Pack16<double> ld16_cs(const double *p) {
   Pack16<double> r;
   r.e[0] = v.x;
   r.e[1] = v.y;
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ Pack16<T> ld16_cs(const T *p) {  // 2-byte types (bf16)
+  const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(p));
+  Pack16<T> r;
+  memcpy(&r, &v, 16);
   return r;
 }
 

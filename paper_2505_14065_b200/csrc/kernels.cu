@@ -242,6 +242,7 @@ extern "C" {
 int pcclb_accumulate(void *acc, const void *in, uint64_t n, int dtype, int op, void *stream) {
   if (!valid_dtype(dtype) || !valid_op(op) || (n && (!acc || !in))) return PCCLB_EINVAL;
   if (dtype == PCCLB_F32) return dispatch_accumulate<float>(acc, in, n, op, as_stream(stream));
+  if (dtype == PCCLB_BF16) return dispatch_accumulate<Bf16>(acc, in, n, op, as_stream(stream));
   return dispatch_accumulate<double>(acc, in, n, op, as_stream(stream));
 }
 
@@ -249,6 +250,7 @@ int pcclb_finalize(void *buf, uint64_t n, int dtype, int op, uint32_t world, voi
   if (!valid_dtype(dtype) || !valid_op(op) || world < 1 || (n && !buf)) return PCCLB_EINVAL;
   if (op != PCCLB_AVG) return PCCLB_OK;
   if (dtype == PCCLB_F32) return launch_div<float>((float *)buf, n, world, as_stream(stream));
+  if (dtype == PCCLB_BF16) return launch_div<Bf16>((Bf16 *)buf, n, world, as_stream(stream));
   return launch_div<double>((double *)buf, n, world, as_stream(stream));
 }
 

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <string.h>
 
 #include <type_traits>
 
@@ -131,6 +132,50 @@ __device__ __forceinline__ T reduce_op(T local, T incoming) {
   } else {
     return x86_add(local, incoming);
   }
+}
+
+// ---------------------------------------------------------------------------
+// bf16 buffers (extension: the reference's collectives take f32/f64 only,
+// collective.py:73-74, so the definition is this repo's, oracle/bf16.py):
+// every fold step computes in f32 with the rules above and rounds the result
+// to bf16 (round to nearest even; a NaN keeps sign and payload, quieted);
+// np.maximum/np.minimum select one of the two bf16 operands unchanged.
+// ---------------------------------------------------------------------------
+struct Bf16 {
+  uint16_t b;
+  Bf16() = default;
+  // the world size as a bf16 (exact for W <= 256)
+  __host__ __device__ explicit Bf16(uint32_t w) {
+    float f = (float)w;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    b = (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+  }
+};
+
+__device__ __forceinline__ float bf16_to_f32(Bf16 x) { return __uint_as_float((uint32_t)x.b << 16); }
+__device__ __forceinline__ Bf16 f32_to_bf16(float f) {
+  const uint32_t u = __float_as_uint(f);
+  Bf16 r;
+  if ((u & 0x7fffffffu) > 0x7f800000u) r.b = (uint16_t)((u >> 16) | 0x0040u);  // NaN: quieted
+  else r.b = (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);              // RNE
+  return r;
+}
+template <>
+__device__ __forceinline__ bool is_nan<Bf16>(Bf16 x) {
+  return (x.b & 0x7fffu) > 0x7f80u;
+}
+
+template <int OP>
+__device__ __forceinline__ Bf16 reduce_op(Bf16 local, Bf16 incoming) {
+  const float a = bf16_to_f32(local), b = bf16_to_f32(incoming);
+  if constexpr (OP == PCCLB_MAX) return (a > b || is_nan(a)) ? local : incoming;
+  else if constexpr (OP == PCCLB_MIN) return (a < b || is_nan(a)) ? local : incoming;
+  else if constexpr (OP == PCCLB_PROD) return f32_to_bf16(x86_mul(a, b));
+  else return f32_to_bf16(x86_add(a, b));
+}
+__device__ __forceinline__ Bf16 div_world(Bf16 x, Bf16 w) {
+  return f32_to_bf16(div_world(bf16_to_f32(x), bf16_to_f32(w)));
 }
 
 // ---------------------------------------------------------------------------

@@ -1534,7 +1534,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const uint32_t own = (rank + 1) % w;  // collective.py:538
   const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
   Signal *me = sig_of(r->ws);
-  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : PCCLB_F32, op, false);
+  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : sizeof(T) == 2 ? PCCLB_BF16 : PCCLB_F32, op, false);
   if (n * sizeof(T) <= small_max_bytes(r)) {
     // latency-bound size: the whole attempt in one kernel (ipc_small_kernel)
     r->last_zero_copy = false;
@@ -2124,6 +2124,8 @@ int pcclb_ring_enqueue(pcclb_ring *r, void *d_buf, uint64_t n, int dtype, int op
       rc = quant_allreduce(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
     else if (dtype == PCCLB_F32)
       rc = plain_allreduce<float>(r, static_cast<float *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
+    else if (dtype == PCCLB_BF16)
+      rc = plain_allreduce<Bf16>(r, static_cast<Bf16 *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
     else
       rc = plain_allreduce<double>(r, static_cast<double *>(d_buf), n, op, attempt, fault_at, timeout_ns, s);
     if (rc) return rc;

@@ -375,6 +375,12 @@ int pcclb_local_allreduce_ex(void *const *h_bufs, uint32_t w, uint64_t n, int dt
       P.n = n, P.w = w, P.avg = avg;
       return local_plain<float>(P, op, vec, grid, s);
     }
+    if (dtype == PCCLB_BF16) {
+      LocalBufs<Bf16> P{};
+      for (uint32_t i = 0; i < w; ++i) P.b[i] = static_cast<Bf16 *>(h_bufs[i]);
+      P.n = n, P.w = w, P.avg = avg;
+      return local_plain<Bf16>(P, op, vec, grid, s);
+    }
     LocalBufs<double> P{};
     for (uint32_t i = 0; i < w; ++i) P.b[i] = static_cast<double *>(h_bufs[i]);
     P.n = n, P.w = w, P.avg = avg;

@@ -173,6 +173,8 @@ class TcpRingEngine:
         op = ReduceOp.parse(op)
         if op is ReduceOp.PROD:
             raise UsageError("PROD is an extension op (north_star): the reference's TCP peers do not implement it")
+        if buffer.dtype == torch.bfloat16:
+            raise UsageError("bf16 is an extension dtype: the reference's frames carry f32/f64 (wire.py DType)")
         if quantize not in (False, True, None, "u8"):
             raise UsageError(f"the TCP frames carry u8 min-max codes only (wire.py QuantMeta), not {quantize!r}")
         if not isinstance(buffer, torch.Tensor) or buffer.dim() != 1 or not buffer.is_contiguous() or not buffer.is_cuda:

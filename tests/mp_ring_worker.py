@@ -248,6 +248,19 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                         eng.run_all_reduce(buf, "prod", quantize=quant)
                         want = oring.ring_allreduce_chunkwise(inputs, oring.ReduceOp.PROD, quantize=quant)
                         check(f"PROD {tag} n={n} q={quant}", buf.cpu().numpy().tobytes() == want.tobytes())
+            # bf16 extension (oracle/bf16.py): small path and multi-kernel schedule
+            from oracle import bf16 as ob
+
+            for n in (1, 4099, 300_007):
+                g_ = np.random.default_rng(n + 5)
+                inputs = [ob.from_f32(g_.normal(0, 1, n).astype(np.float32)) for _ in range(world)]
+                for eng, tag in ((ring, "small"), (multi, "multi-kernel")):
+                    for op in ("avg", "max"):
+                        buf = torch.from_numpy(inputs[eng.position].view(np.int16).copy()).to(dev).view(torch.bfloat16)
+                        eng.run_all_reduce(buf, op)
+                        want = ob.ring_allreduce_chunkwise(inputs, oring.ReduceOp[op.upper()])
+                        got = buf.view(torch.int16).cpu().numpy().view(np.uint16)
+                        check(f"bf16 {tag} n={n} {op}", got.tobytes() == want.tobytes())
             multi.close()
         if "large" in scenarios or "large_small" in scenarios:
             n = (1 << 24) + 3 if "large" in scenarios else (1 << 21) + 3

@@ -178,3 +178,53 @@ def test_qformat_rejected_by_nvlink_and_tcp_engines():
     with pytest.raises(UsageError):
         qformat_code("fp8")
     del UsageError
+
+
+# ---------------------------------------------------------------------------
+# bf16 buffers (oracle/bf16.py): f32 arithmetic per fold step, RNE to bf16
+# ---------------------------------------------------------------------------
+def _bf16_inputs(w, n, seed, op):
+    from oracle import bf16 as ob
+
+    rng = np.random.default_rng(seed)
+    if op == "prod":
+        fl = [(1.0 + 0.05 * rng.normal(0, 1, n)).astype(np.float32) for _ in range(w)]
+    else:
+        fl = [rng.normal(0, 1, n).astype(np.float32) for _ in range(w)]
+    out = [ob.from_f32(f) for f in fl]
+    if n > 8:
+        out[0][:3] = [0x0000, 0x8000, 0x7F80]  # +0, -0, +inf
+    return out
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("n", [1, 7, 4099, 100_003])
+@pytest.mark.parametrize("op", ["sum", "avg", "max", "min", "prod"])
+def test_bf16_local_ring(w, n, op):
+    from oracle import bf16 as ob
+    from paper_2505_14065_b200 import LocalRing
+
+    host = _bf16_inputs(w, n, 7 * n + w, op)
+    want = ob.ring_allreduce_chunkwise(host, oring.ReduceOp[op.upper()]) if w > 1 else (
+        ob.from_f32(ob.to_f32(host[0]) / np.float32(1)) if op == "avg" else host[0])
+    dev = [torch.from_numpy(h.view(np.int16).copy()).cuda().view(torch.bfloat16) for h in host]
+    res = LocalRing(w).run_op(dev, op)
+    assert all(s == "ok" for s, _ in res)
+    for d in dev:
+        assert d.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("op", ["sum", "max", "prod"])
+def test_bf16_accumulate_and_finalize(op):
+    from oracle import bf16 as ob
+    from paper_2505_14065_b200.collective import accumulate, finalize_reduction
+
+    a, b = _bf16_inputs(2, 100_001, 3, op)
+    da = torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    db = torch.from_numpy(b.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    accumulate(op, da, db)
+    want = ob.accumulate(oring.ReduceOp[op.upper()], a, b)
+    assert da.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == want.tobytes()
+    finalize_reduction(da, "avg", 3)
+    want = ob.from_f32(ob.to_f32(want) / np.float32(3))
+    assert da.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == want.tobytes()
