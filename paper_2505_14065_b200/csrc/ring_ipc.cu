@@ -77,7 +77,13 @@ constexpr uint64_t kSignalBytes = 16384;
 constexpr int kIpcThreads = 512;
 constexpr uint64_t kQB = PCCLB_QB;  // elements per ready-flag block of the fused quantized steps
 // fused gather blocks: larger (fewer release fences; measured W=2: 64 Ki 1.92 ms, 256 Ki 1.80 ms)
-constexpr uint64_t kQF = 4 * kQB;
+#ifndef PCCLB_QF_MUL
+#define PCCLB_QF_MUL 4
+#endif
+#ifndef PCCLB_QF_U
+#define PCCLB_QF_U 2
+#endif
+constexpr uint64_t kQF = PCCLB_QF_MUL * kQB;
 #ifndef PCCLB_QTHREADS
 #define PCCLB_QTHREADS 256
 #endif
@@ -1235,10 +1241,10 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(cons
       // for an overflowed range, scale = inf)
       if (finite_f(qp.scale) && finite_f(qp.mn)) {
         QuantPushF<false> f{&a, a.buf + olo, qp, coff};
-        cta_loop16<2>(olo, i0, i1, a.vec != 0, f);
+        cta_loop16<PCCLB_QF_U>(olo, i0, i1, a.vec != 0, f);
       } else {
         QuantPushF<true> f{&a, a.buf + olo, qp, coff};
-        cta_loop16<2>(olo, i0, i1, a.vec != 0, f);
+        cta_loop16<PCCLB_QF_U>(olo, i0, i1, a.vec != 0, f);
       }
       __syncthreads();
       if (threadIdx.x < w && threadIdx.x != a.rank) {
@@ -1258,10 +1264,10 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(cons
       const float mn = m->min_val, sc = m->scale;
       if (finite_f(sc) && finite_f(mn)) {
         Dequant16T<false> f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
-        cta_loop16<2>(clo, i0, i1, a.vec != 0, f);
+        cta_loop16<PCCLB_QF_U>(clo, i0, i1, a.vec != 0, f);
       } else {
         Dequant16F f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
-        cta_loop16<2>(clo, i0, i1, a.vec != 0, f);
+        cta_loop16<PCCLB_QF_U>(clo, i0, i1, a.vec != 0, f);
       }
     }
   }
