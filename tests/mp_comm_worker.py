@@ -30,6 +30,7 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
     from oracle import simplehash as osh
     from paper_2505_14065_b200.collective import UsageError
     from paper_2505_14065_b200.communicator import Communicator, SyncStatus
+    from paper_2505_14065_b200.ring_ipc import DeviceRing
     from paper_2505_14065_b200.sharedstate import DType, SharedStateEntry
 
     dev = torch.device("cuda", gpu)
@@ -136,6 +137,89 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             check("size mismatch: error", res.status is SyncStatus.ERROR, res)
             check("size mismatch: untouched", bool((odd == rank).all()))
             comm.close()
+
+        if "sync_scale" in scenarios:
+            # config 4 at size: every rank holds the 16.06 GB Llama-3-8B-like state;
+            # the drifted peer has one flipped bit in the 1.05 GB embedding at equal
+            # revision; one sync restores bit parity (a single entry moves)
+            import time
+
+            from bench import llama3_8b_layout
+
+            layout = llama3_8b_layout()
+            total = sum(n_ for _, n_ in layout)
+            state = torch.empty(total, dtype=torch.bfloat16, device=dev)
+            gen = torch.Generator(device=dev).manual_seed(77)
+            state.view(torch.int16).random_(-32768, 32767, generator=gen)
+            views, off = [], 0
+            for _, n_ in layout:
+                views.append(state[off: off + n_])
+                off += n_
+            clean = [osh_u for osh_u in []]  # filled below from the device digests
+            from paper_2505_14065_b200 import simplehash_many
+
+            clean = simplehash_many(views)
+            drifted = 1 % world
+            if rank == drifted:
+                views[0].view(torch.int16)[12345] ^= 1
+            entries = [SharedStateEntry(name, DType.U8, v.view(torch.uint8), revision=3)
+                       for (name, _), v in zip(layout, views)]
+            comm = Communicator(device=dev, pool_size=1, timeout_s=60.0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            res = comm.sync_shared_state(entries)
+            dt = time.perf_counter() - t0
+            if world >= 3:
+                check("sync 16 GB: updated", res.status in (SyncStatus.UPDATED,), res)
+                check("sync 16 GB: popular state everywhere", simplehash_many(views) == clean)
+                check("sync 16 GB: one entry moved", rank != drifted or comm.stats["sync_payload_rx"] == views[0].numel() * 2,
+                      comm.stats["sync_payload_rx"])
+            else:  # two peers: the smaller hash wins the tie
+                got = simplehash_many(views)
+                alls = [None] * world
+                dist.all_gather_object(alls, got)
+                check("sync 16 GB: digest parity", all(a == got for a in alls))
+            check(f"sync 16 GB: {dt:.2f} s host time", dt < 30.0, dt)
+            comm.close()
+            del state, views, entries
+            torch.cuda.empty_cache()
+
+        if "churn_scale" in scenarios and world >= 3:
+            # config 5 at size: two concurrent u8 AVG all-reduces of 600 M f32 each
+            # (tags 0 and 1); the dropped peer never enqueues tag 1: tag 0 completes
+            # bit-exact (own chunk against the oracle), tag 1 aborts and restores
+            n = 600_000_000
+            comm = Communicator(device=dev, pool_size=2, timeout_s=10.0,
+                                capacity_bytes=DeviceRing.required_bytes(n, world, 4, True))
+
+            def gen_(p, seed):
+                g_ = torch.Generator(device=dev).manual_seed(seed + p)
+                return torch.randn(n, generator=g_, device=dev) * 1e-2
+
+            b0, b1 = gen_(rank, 100), gen_(rank, 200)
+            src1 = b1.clone()
+            dropped = world - 1
+            torch.cuda.synchronize()
+            dist.barrier()
+            h0 = comm.all_reduce_async(b0, 0, "avg", quantize=True)
+            if rank != dropped:
+                h1 = comm.all_reduce_async(b1, 1, "avg", quantize=True)
+            r0 = comm.await_async_reduce(h0)
+            check("churn 600M: tag0 completed", r0.completed, r0)
+            bounds = oring.chunk_bounds(n, world)
+            c = (rank + 1) % world
+            lo, hi = bounds[c]
+            spans = [gen_((c + k) % world, 100)[lo:hi].cpu().numpy() for k in range(world)]
+            want = oring.reduce_chunk(spans, oring.ReduceOp.AVG, True, world)
+            check("churn 600M: tag0 own chunk exact", b0[lo:hi].cpu().numpy().tobytes() == want.tobytes())
+            del spans, want
+            if rank != dropped:
+                r1 = comm.await_async_reduce(h1)
+                check("churn 600M: tag1 aborted", not r1.completed, r1)
+                check("churn 600M: tag1 restored", bool(torch.equal(b1, src1)))
+            comm.close()
+            dist.barrier()
 
         if "churn" in scenarios and world >= 3:
             # config 5: tags 0 and 1 (two halves of a pseudo-gradient), u8 AVG, in flight together
