@@ -91,19 +91,29 @@ __device__ __forceinline__ uint32_t crc_bytes(const uint32_t (*T)[256], uint32_t
   return c;
 }
 
-// one 8-byte slice-by-8 step
-__device__ __forceinline__ uint32_t crc_step8(const uint32_t (*T)[256], uint32_t c, uint32_t lo, uint32_t hi) {
+// one 8-byte slice-by-8 step on the replicated tables: entry i of table s,
+// copy r sits at word ((s * 256 + i) * kCrcCopies + r); a lane reads copy
+// lane % kCrcCopies, so the 32 lanes of a lookup spread over
+// (entry * kCrcCopies + copy) mod 32 banks (random entries: ~1.6 instead of
+// ~3.5 wavefronts per lookup)
+constexpr int kCrcCopies = 8;
+__device__ __forceinline__ uint32_t crc_step8r(const uint32_t *T, uint32_t r, uint32_t c, uint32_t lo, uint32_t hi) {
   c ^= lo;
-  return T[7][c & 0xff] ^ T[6][(c >> 8) & 0xff] ^ T[5][(c >> 16) & 0xff] ^ T[4][c >> 24] ^ T[3][hi & 0xff] ^
-         T[2][(hi >> 8) & 0xff] ^ T[1][(hi >> 16) & 0xff] ^ T[0][hi >> 24];
+#define CRC_T(s, i) T[(((s) * 256u + (i)) * kCrcCopies) + r]
+  return CRC_T(7, c & 0xff) ^ CRC_T(6, (c >> 8) & 0xff) ^ CRC_T(5, (c >> 16) & 0xff) ^ CRC_T(4, c >> 24) ^
+         CRC_T(3, hi & 0xff) ^ CRC_T(2, (hi >> 8) & 0xff) ^ CRC_T(1, (hi >> 16) & 0xff) ^ CRC_T(0, hi >> 24);
+#undef CRC_T
 }
 
+constexpr int kCrcSmem = 8 * 256 * kCrcCopies * 4;
+
 __global__ void __launch_bounds__(kCrcThreads) crc32_seg_kernel(const __grid_constant__ CrcBatch b, uint32_t *seg_raw) {
-  __shared__ uint32_t T[8][256];
+  extern __shared__ uint32_t TR[];  // 8 tables x 256 entries x kCrcCopies
   __shared__ uint32_t s_red[kCrcThreads / 32];
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&T[0][0])[i] = (&c_crc.table[0][0])[i];
+  for (int i = threadIdx.x; i < 8 * 256 * kCrcCopies; i += blockDim.x) TR[i] = (&c_crc.table[0][0])[i / kCrcCopies];
   __syncthreads();
-  const uint32_t t = threadIdx.x;
+  const uint32_t t = threadIdx.x, rcopy = t % kCrcCopies;
+  const uint32_t(*T)[256] = reinterpret_cast<const uint32_t(*)[256]>(&c_crc.table[0][0]);  // byte tail path
   for (uint32_t item = blockIdx.x; item < b.items; item += gridDim.x) {
     // entry of the item (entries hold consecutive item ranges)
     uint32_t lo = 0, hi = b.count;
@@ -124,8 +134,8 @@ __global__ void __launch_bounds__(kCrcThreads) crc32_seg_kernel(const __grid_con
 #pragma unroll 4
       for (uint32_t i = 0; i < kCrcPerThread / 16; ++i) {
         const uint4 v = __ldcs(q + i);
-        c = crc_step8(T, c, v.x, v.y);
-        c = crc_step8(T, c, v.z, v.w);
+        c = crc_step8r(TR, rcopy, c, v.x, v.y);
+        c = crc_step8r(TR, rcopy, c, v.z, v.w);
       }
     } else {
       c = crc_bytes(T, c, p, len);
@@ -214,6 +224,9 @@ int pcclb_crc32_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, uint3
   int rc = crc_init_constants();
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
+  static const cudaError_t attr = cudaFuncSetAttribute(crc32_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       kCrcSmem);
+  if (attr != cudaSuccess) return cuda_status(attr);
   static thread_local CrcBatch batch;
   for (uint32_t base = 0; base < count; base += kCrcMaxEntries) {
     const uint32_t m = std::min<uint32_t>(kCrcMaxEntries, count - base);
@@ -234,7 +247,7 @@ int pcclb_crc32_multi(const void *const *h_ptrs, const uint64_t *h_nbytes, uint3
     if (items) PCCLB_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&seg_raw), items * sizeof(uint32_t), s));
     if (items) {
       const unsigned grid = (unsigned)std::min<uint64_t>(items, (uint64_t)sm_count() * 8);
-      crc32_seg_kernel<<<grid, kCrcThreads, 0, s>>>(batch, seg_raw);
+      crc32_seg_kernel<<<grid, kCrcThreads, kCrcSmem, s>>>(batch, seg_raw);
       PCCLB_LAUNCH_CHECK();
     }
     crc32_combine_kernel<<<m, 1024, 0, s>>>(batch, seg_raw);

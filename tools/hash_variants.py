@@ -56,6 +56,8 @@ res["config4_rest"], _ = timeit(views[1:-1], 5)
 res["single_1GB"], _ = timeit([views[0]], 5)
 eq = state[: 64 * (32 << 20)].view(64, -1)
 res["64x64MiB"], _ = timeit([eq[i] for i in range(64)], 7)
+if os.environ.get("HASH_SINGLE_16G"):  # config 4's single-entry stress case (the whole state as one entry)
+    res["single_16GB"], _ = timeit([state.view(torch.uint8)], 3)
 res["digest0"] = digests[0] & 0xFFFFFFFFFFFFFFFF
 print(json.dumps(res), flush=True)
 try:
