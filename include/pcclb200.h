@@ -233,7 +233,7 @@ PCCLB_API volatile uint64_t *pcclb_ring_abort_word(pcclb_ring *r);
 PCCLB_API int pcclb_ring_set_slots(pcclb_ring *r, uint32_t slots);
 /* Plain ops of at most `bytes` run as one fused kernel (copy-in, arrival,
  * local fold of every chunk in its ring order, completion vote): the
- * latency-bound end of the config-2 sweep. Default 32 MiB / W
+ * latency-bound end of the config-2 sweep. Default 64 MiB at W = 2, else 32 MiB / W
  * (PCCLB_SMALL_MAX overrides); 0 disables. Every rank of a ring must use the same value (the
  * path is part of the parameter check at the arrival). */
 PCCLB_API int pcclb_ring_set_small_max(pcclb_ring *r, uint64_t bytes);

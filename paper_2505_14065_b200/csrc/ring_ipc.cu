@@ -1417,9 +1417,12 @@ uint64_t small_max_bytes(const pcclb_ring *r) {
   }();
   if (env >= 0) return (uint64_t)env;
   // the small path's NVLink ingress is (W-1)*N against the ring's 2(W-1)/W*N:
-  // equal at W=2, W/2 times more beyond (W=2 measured: 1 MiB 29.9 vs 55.6 us,
-  // 4 MiB 33.2 vs 62.2 us on the multi-kernel schedule)
-  return (32ull << 20) / (r->world ? r->world : 1);
+  // equal at W=2, W/2 times more beyond. Measured (bench.py --workload sweep,
+  // small path vs multi-kernel schedule): W=2 1 MiB 32 vs 57 us, 16 MiB 59 vs
+  // 85, 64 MiB 157 vs 167, 256 MiB 542 vs 476; W=4 4 MiB 68 vs 74, 16 MiB
+  // 144 vs 110
+  const uint32_t w = r->world ? r->world : 1;
+  return w == 2 ? (64ull << 20) : (32ull << 20) / w;
 }
 // co-resident grid (the CTAs wait for each other): one CTA per 8 Ki elements, at most 128
 unsigned small_grid(uint64_t n) {
