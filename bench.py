@@ -227,7 +227,9 @@ def bench_hash(args, rank, world, local):
     clk = clocks.stop()
     barrier(world)
     ms_max = max_over_ranks(ms, world)
-    launches = 2 * args.steps  # per step: the batch kernel + the big-entry kernel
+    # per step: the batch kernel, the big-entry kernel and the 1-CTA gate
+    # kernel between them (replayed as one CUDA graph of the plan)
+    launches = 3 * args.steps
 
     # the two 1.05 GB entries alone (the bitsliced big-entry kernel) and the
     # other 289 alone (the TMA batch kernel): how the concurrent launch overlaps
