@@ -88,7 +88,10 @@ constexpr uint64_t kQF = PCCLB_QF_MUL * kQB;
 #define PCCLB_QTHREADS 256
 #endif
 constexpr int kQThreads = PCCLB_QTHREADS;
-constexpr int kQMinBlocks = 1024 / kQThreads;  // 64 registers per thread
+#ifndef PCCLB_QMINB
+#define PCCLB_QMINB (1024 / PCCLB_QTHREADS)
+#endif
+constexpr int kQMinBlocks = PCCLB_QMINB;  // default 4 x 256 threads: 64 registers per thread
 
 struct Signal {
   uint64_t arrive[kIpcMaxWorld];     // written by peer j: its latest barrier token
@@ -915,10 +918,11 @@ __global__ void __launch_bounds__(kIpcThreads, 2)
 //      to the successor -- here pushed over NVLink into the successor's
 //      codes[s] with remote 16-byte stores, 64 Ki elements per block, each
 //      block followed by a ready token (st.release.sys) in its flags[s];
-//   B: buf[rx_s] <- buf[rx_s] (+) D(pred's codes[s]) for each block once the
-//      predecessor's token for it is visible (ld.acquire.sys), saving the old
-//      values (first touch of the rx chunk = the backup) and accumulating the
-//      range of the new partial for step s+1's quantization.
+//   B: for each block once the predecessor's token for it is visible
+//      (ld.acquire.sys): save buf[rx_s] (first touch of the rx chunk = the
+//      backup) and accumulate the range of the partial buf[rx_s] (+) D(pred's
+//      codes[s]) for step s+1's quantization. The partial itself is not
+//      stored: step s+1's A (or the owner's adoption) recomputes it.
 // Work items are claimed in order from a per-step counter, A block j at
 // position 2j and B block j at 2j + 2*lag + 1, the same positions on every
 // rank. A items never wait, so a claimed B item always has its producer's A
@@ -936,6 +940,8 @@ struct QStepArgs {
   pcclb_qmeta *tmeta;         // successor's qmeta[s]
   uint64_t *tflags;           // successor's flags[s]
   const pcclb_range *trange;  // range of the tx chunk (previous step)
+  const uint8_t *pcodes;      // step >= 1: own codes[s-1] at element 0 of the tx chunk (the
+  const pcclb_qmeta *pmeta;   //   tx chunk's partial is buf (+) D(codes[s-1]), never stored)
   float *rx;                  // rx chunk (caller buffer)
   float *rbak;                // backup of the rx chunk
   const uint8_t *rcodes;      // own codes[s] at element 0 of the rx chunk
@@ -1032,6 +1038,121 @@ __device__ __forceinline__ void cta_loop16(uint64_t lo, uint64_t i0, uint64_t i1
   if (t0 + t < i1) f.one(t0 + t);
 }
 
+// the same with 4-element vectors (lane-contiguous 16-byte accesses)
+template <int U, typename F>
+__device__ __forceinline__ void cta_loop4(uint64_t lo, uint64_t i0, uint64_t i1, bool vec, F &f) {
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  if (!vec) {
+    for (uint64_t i = i0 + t; i < i1; i += nt) f.one(i);
+    return;
+  }
+  uint64_t head = (4 - ((lo + i0) & 3)) & 3;
+  if (head > i1 - i0) head = i1 - i0;
+  if (t < head) f.one(i0 + t);
+  const uint64_t b = i0 + head;
+  const uint64_t nv = (i1 - b) / 4;
+  uint64_t v = t;
+  for (; v + (U - 1) * nt < nv; v += U * nt) {
+    typename F::In in[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) in[u] = f.vload(b + (v + u * nt) * 4);
+#pragma unroll
+    for (int u = 0; u < U; ++u) f.vapply(b + (v + u * nt) * 4, in[u]);
+  }
+  for (; v < nv; v += nt) {
+    typename F::In in = f.vload(b + v * 4);
+    f.vapply(b + v * 4, in);
+  }
+  const uint64_t t0 = b + nv * 4;
+  if (t0 + t < i1) f.one(t0 + t);
+}
+
+#ifndef PCCLB_QB_U
+#define PCCLB_QB_U 8
+#endif
+#ifndef PCCLB_QR_U
+#define PCCLB_QR_U 4
+#endif
+
+// The running partial of a chunk is never written back to the caller's
+// buffer: the consumer of step s only saves the backup and accumulates the
+// range of buf[rx] (+) D(codes[s]); whoever needs the partial next (the
+// producer of step s+1, or the owner's adoption) recomputes it from the same
+// two inputs with the same arithmetic -- 5 bytes read instead of a 4-byte
+// write plus a 4-byte read per element and step.
+template <int OP>
+__device__ __forceinline__ float partial_of(float local, uint32_t q, float mn, float scale) {
+  return reduce_op_x<OP, false>(local, dequant1x<false>(q, mn, scale));
+}
+
+// consumer of a step: bak <- buf[rx], range of buf[rx] (+) D(codes)
+template <int OP>
+struct DequantRange4F {
+  const float *__restrict__ acc;
+  const uint8_t *__restrict__ codes;
+  float mn, scale;
+  RangeAcc r;
+  float *__restrict__ bak;
+  __device__ __forceinline__ void one(uint64_t i) {
+    const float old = acc[i];
+    bak[i] = old;
+    r.add(partial_of<OP>(old, __ldcg(codes + i), mn, scale));
+  }
+  struct In {
+    Pack16<float> a;
+    uint32_t q;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) {
+    In v;
+    v.a = ld16(acc + i);
+    v.q = __ldcg(reinterpret_cast<const uint32_t *>(codes + i));
+    return v;
+  }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    st16(bak + i, v.a);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r.add(partial_of<OP>(v.a.e[k], (v.q >> (8 * k)) & 0xffu, mn, scale));
+  }
+};
+
+// producer of step s >= 1: codes <- Q(buf[tx] (+) D(codes[s-1]))
+template <int OP>
+struct QuantPart16F {
+  const float *__restrict__ x;
+  const uint8_t *__restrict__ pcodes;
+  float pmn, pscale;
+  uint8_t *__restrict__ codes;
+  QParams qp;
+  __device__ __forceinline__ void one(uint64_t i) {
+    const float v = partial_of<OP>(x[i], __ldcg(pcodes + i), pmn, pscale);
+    codes[i] = (uint8_t)quant1_fast(v, qp.mn, qp.scale, qp.inv);
+  }
+  struct In {
+    Pack16<float> a[4];
+    uint4 p;
+  };
+  __device__ __forceinline__ In vload(uint64_t i) {
+    In v;
+    v.p = __ldcg(reinterpret_cast<const uint4 *>(pcodes + i));
+#pragma unroll
+    for (int g = 0; g < 4; ++g) v.a[g] = ld16(x + i + 4 * g);
+    return v;
+  }
+  __device__ __forceinline__ void vapply(uint64_t i, const In &v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint32_t q[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        q[k] = quant1_fast(partial_of<OP>(v.a[g].e[k], code_byte(v.p, 4 * g + k), pmn, pscale), qp.mn, qp.scale,
+                           qp.inv);
+      w[g] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    }
+    *reinterpret_cast<uint4 *>(codes + i) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
 template <int OP>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qstep_kernel(const __grid_constant__ QStepArgs a) {
   __shared__ uint32_t s_item, s_ok;
@@ -1071,8 +1192,15 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qstep_kernel(const
       const uint64_t j = it / 2;
       if (j >= nA || !ok) continue;
       qblock_range(a.tlo, a.tn, j, i0, i1);
-      Quant16F f{a.tx, (a.dbg & 2) ? const_cast<uint8_t *>(a.rcodes) : a.tcodes, nullptr, qp, 1.0f, false};
-      cta_loop16<2>(a.tlo, i0, i1, a.tvec != 0, f);
+      uint8_t *dst = (a.dbg & 2) ? const_cast<uint8_t *>(a.rcodes) : a.tcodes;
+      if (a.pcodes) {
+        const volatile pcclb_qmeta *pm = a.pmeta;
+        QuantPart16F<OP> f{a.tx, a.pcodes, pm->min_val, pm->scale, dst, qp};
+        cta_loop16<2>(a.tlo, i0, i1, a.tvec != 0, f);
+      } else {
+        Quant16F f{a.tx, dst, nullptr, qp, 1.0f, false};
+        cta_loop16<2>(a.tlo, i0, i1, a.tvec != 0, f);
+      }
       __syncthreads();  // every thread's remote stores precede the token
       if (threadIdx.x == 0) {
         volatile pcclb_qmeta *m = a.tmeta;
@@ -1093,8 +1221,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qstep_kernel(const
       }
       const volatile pcclb_qmeta *m = a.rmeta;
       // plain arithmetic: a NaN here makes the next range non-finite -> abort + restore
-      DequantAcc16F<OP, false> f{a.rx, a.rcodes, m->min_val, m->scale, racc, a.rbak};
-      cta_loop16<2>(a.rlo, i0, i1, a.rvec != 0, f);
+      DequantRange4F<OP> f{a.rx, a.rcodes, m->min_val, m->scale, racc, a.rbak};
+      cta_loop4<PCCLB_QR_U>(a.rlo, i0, i1, a.rvec != 0, f);
       racc = f.r;
     }
   }
@@ -1104,7 +1232,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qstep_kernel(const
 // ---------------------------------------------------------------------------
 // Fused gather (quantized): the owner's adoption and the W-1 dequantizing
 // copies in one kernel, without the barrier between them.
-//   A' (owner of chunk own = rank+1, collective.py:538-551): codes <- Q(own)
+//   A' (owner of chunk own = rank+1, collective.py:538-551): codes <- Q(own),
+//      own = buf[own] (+) D(codes[W-2]) recomputed (see partial_of),
 //      with the last step's range, own <- D(codes) / W in place, and the codes
 //      pushed into every peer's gcodes[own] (remote 16-byte stores), one
 //      ready token per 64 Ki-element block in each peer's gflags[own];
@@ -1119,6 +1248,8 @@ struct QFinalArgs {
   float *buf;
   uint64_t lo[kIpcMaxWorld + 1];  // chunk bounds: chunk c = [lo[c], lo[c+1])
   const pcclb_range *orange;      // range of the own chunk's final partial
+  const uint8_t *ocodes;          // own codes[W-2] at element 0 of the own chunk: the final
+  const pcclb_qmeta *ometa;       //   partial is buf[own] (+) D(ocodes) (never stored)
   uint64_t gcodes_off, codes_stride, gflags_off, flags_stride;  // workspace offsets (same on every rank)
   Signal *mine;
   Signal *peer[kIpcMaxWorld];     // peer workspaces (Signal at offset 0)
@@ -1129,7 +1260,7 @@ struct QFinalArgs {
   float avg;  // 1: no division
   uint32_t do_div;
   uint32_t dbg;  // experiments (PCCLB_QDEBUG bits): 1 B' never waits, 4 A' pushes to its own
-                 // workspace, 8 B' items skipped
+                 // workspace, 8 B' items skipped, 16 A' posts no tokens, 32 A' items skipped
 };
 
 __device__ __forceinline__ uint8_t *gcodes_of(const QFinalArgs &a, Signal *ws, uint32_t c) {
@@ -1139,28 +1270,33 @@ __device__ __forceinline__ uint64_t *gflags_of(const QFinalArgs &a, Signal *ws, 
   return reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(ws) + a.gflags_off + c * a.flags_stride);
 }
 
-// quantize + adopt in place + push the codes to every peer
-template <bool X86>
+// recompute the final partial, quantize + adopt in place + push the codes to
+// every peer
+template <bool X86, int OP>
 struct QuantPushF {
   const QFinalArgs *a;
   float *x;
   QParams qp;
   uint64_t coff;  // chunk's code offset inside a peer's workspace
+  const uint8_t *pcodes;
+  float pmn, pscale;
   __device__ __forceinline__ float adopt_val(uint32_t q) {
     float d = dequant1x<X86>(q, qp.mn, qp.scale);
     return a->do_div ? div_world_x<X86>(d, a->avg) : d;
   }
   __device__ __forceinline__ void one(uint64_t i) {
-    const uint32_t q = quant1_fast(x[i], qp.mn, qp.scale, qp.inv);
+    const uint32_t q = quant1_fast(partial_of<OP>(x[i], __ldcg(pcodes + i), pmn, pscale), qp.mn, qp.scale, qp.inv);
     x[i] = adopt_val(q);
     for (uint32_t p = 0; p < a->world; ++p)
       if (p != a->rank) (reinterpret_cast<uint8_t *>(a->peer[p]) + coff)[i] = (uint8_t)q;
   }
   struct In {
     Pack16<float> v[4];
+    uint4 p;
   };
   __device__ __forceinline__ In vload(uint64_t i) {
     In r;
+    r.p = __ldcg(reinterpret_cast<const uint4 *>(pcodes + i));
 #pragma unroll
     for (int g = 0; g < 4; ++g) r.v[g] = ld16(x + i + 4 * g);
     return r;
@@ -1173,7 +1309,8 @@ struct QuantPushF {
       Pack16<float> d;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        q[k] = quant1_fast(in.v[g].e[k], qp.mn, qp.scale, qp.inv);
+        q[k] = quant1_fast(partial_of<OP>(in.v[g].e[k], code_byte(in.p, 4 * g + k), pmn, pscale), qp.mn, qp.scale,
+                           qp.inv);
         d.e[k] = adopt_val(q[k]);
       }
       w[g] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
@@ -1186,6 +1323,7 @@ struct QuantPushF {
   }
 };
 
+template <int OP>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(const __grid_constant__ QFinalArgs a) {
   __shared__ uint32_t s_item, s_ok;
   const uint32_t w = a.world, own = a.own;
@@ -1234,20 +1372,22 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(cons
     const uint64_t r = it / w;
     uint64_t i0, i1;
     if (k == 0) {
-      if (r >= nO) continue;
+      if (r >= nO || (a.dbg & 32)) continue;
       qblock_range(olo, on, r, i0, i1, kQF);
       const uint64_t coff = a.gcodes_off + own * a.codes_stride + olo % 16;
       // finite scale and min: no NaN can arise (the x86 NaN rules only matter
       // for an overflowed range, scale = inf)
+      const volatile pcclb_qmeta *pm = a.ometa;
+      const float pmn = pm->min_val, psc = pm->scale;
       if (finite_f(qp.scale) && finite_f(qp.mn)) {
-        QuantPushF<false> f{&a, a.buf + olo, qp, coff};
+        QuantPushF<false, OP> f{&a, a.buf + olo, qp, coff, a.ocodes, pmn, psc};
         cta_loop16<PCCLB_QF_U>(olo, i0, i1, a.vec != 0, f);
       } else {
-        QuantPushF<true> f{&a, a.buf + olo, qp, coff};
+        QuantPushF<true, OP> f{&a, a.buf + olo, qp, coff, a.ocodes, pmn, psc};
         cta_loop16<PCCLB_QF_U>(olo, i0, i1, a.vec != 0, f);
       }
       __syncthreads();
-      if (threadIdx.x < w && threadIdx.x != a.rank) {
+      if (threadIdx.x < w && threadIdx.x != a.rank && !(a.dbg & 16)) {
         Signal *p = a.peer[threadIdx.x];
         volatile pcclb_qmeta *m = &p->gmeta[own];
         m->min_val = qp.mn;
@@ -1263,8 +1403,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks) ipc_qfinal_kernel(cons
       const volatile pcclb_qmeta *m = &a.mine->gmeta[c];
       const float mn = m->min_val, sc = m->scale;
       if (finite_f(sc) && finite_f(mn)) {
-        Dequant16T<false> f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
-        cta_loop16<PCCLB_QF_U>(clo, i0, i1, a.vec != 0, f);
+        Dequant4T<false> f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
+        cta_loop4<PCCLB_QB_U>(clo, i0, i1, a.vec != 0, f);
       } else {
         Dequant16F f{a.buf + clo, gcodes_of(a, a.mine, c), mn, sc, a.avg, a.do_div != 0};
         cta_loop16<PCCLB_QF_U>(clo, i0, i1, a.vec != 0, f);
@@ -1543,7 +1683,7 @@ int plain_allreduce(pcclb_ring *r, T *buf, uint64_t n, int op, uint64_t attempt,
   const uint32_t own = (rank + 1) % w;  // collective.py:538
   const uint64_t own_lo = lo[2 * own], own_n = lo[2 * own + 1] - lo[2 * own];
   Signal *me = sig_of(r->ws);
-  uint64_t desc = param_tag(n, sizeof(T) == 8 ? PCCLB_F64 : sizeof(T) == 2 ? PCCLB_BF16 : PCCLB_F32, op, false);
+  uint64_t desc = param_tag(n, sizeof(T) == 8 ? (int)PCCLB_F64 : sizeof(T) == 2 ? (int)PCCLB_BF16 : (int)PCCLB_F32, op, false);
   if (n * sizeof(T) <= small_max_bytes(r)) {
     // latency-bound size: the whole attempt in one kernel (ipc_small_kernel)
     r->last_zero_copy = false;
@@ -1832,6 +1972,8 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
       q.tmeta = &sig_of(r->peer_ws[succ])->qmeta[step];
       q.tflags = reinterpret_cast<uint64_t *>(r->peer_ws[succ] + L.flags_step(step));
       q.trange = &me->range[step];
+      q.pcodes = step ? reinterpret_cast<const uint8_t *>(r->ws + codes_at(L.codes_step(step - 1), q.tlo)) : nullptr;
+      q.pmeta = step ? &me->qmeta[step - 1] : nullptr;
       q.rx = buf + q.rlo;
       q.rbak = bak + q.rlo;
       q.rcodes = reinterpret_cast<const uint8_t *>(r->ws + codes_at(L.codes_step(step), q.rlo));
@@ -1906,6 +2048,8 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     for (uint32_t c = 0; c < w; ++c) g.lo[c] = lo[2 * c];
     g.lo[w] = n;
     g.orange = &me->range[w - 1];
+    g.ocodes = reinterpret_cast<const uint8_t *>(r->ws + codes_at(L.codes_step(w - 2), lo[2 * own]));
+    g.ometa = &me->qmeta[w - 2];
     g.gcodes_off = L.gcodes;
     g.codes_stride = L.codes_stride;
     g.gflags_off = L.gflags;
@@ -1931,7 +2075,20 @@ int quant_allreduce(pcclb_ring *r, float *buf, uint64_t n, int op, uint64_t atte
     g.vec = (reinterpret_cast<uintptr_t>(buf) & 63) == 0 ? 1u : 0u;
     g.avg = (op == PCCLB_AVG) ? (float)w : 1.0f;
     g.do_div = op == PCCLB_AVG ? 1u : 0u;
-    ipc_qfinal_kernel<<<grid, kQThreads, 0, s>>>(g);
+    switch (op) {
+      case PCCLB_MAX:
+        ipc_qfinal_kernel<PCCLB_MAX><<<grid, kQThreads, 0, s>>>(g);
+        break;
+      case PCCLB_MIN:
+        ipc_qfinal_kernel<PCCLB_MIN><<<grid, kQThreads, 0, s>>>(g);
+        break;
+      case PCCLB_PROD:
+        ipc_qfinal_kernel<PCCLB_PROD><<<grid, kQThreads, 0, s>>>(g);
+        break;
+      default:
+        ipc_qfinal_kernel<PCCLB_SUM><<<grid, kQThreads, 0, s>>>(g);
+        break;
+    }
     PCCLB_LAUNCH_CHECK();
     r->timer.mark(s);
     rc = launch_vote_and_restore(r, buf, n * sizeof(float), attempt, w, fault_at, timeout_ns, s);

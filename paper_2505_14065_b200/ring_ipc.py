@@ -159,6 +159,15 @@ class DeviceRing:
         esz = torch.tensor([], dtype=dtype).element_size()
         self._create(self.required_bytes(n, self.world, esz, quantize))
 
+    def set_small_max_bytes(self, nbytes: int | None) -> None:
+        """Largest op (bytes) that takes the one-kernel small path; None = the
+        engine default. Every rank must set the same value (the path is part
+        of the op descriptor the barrier compares)."""
+        self.small_max_bytes = nbytes
+        if self._handle:
+            check(lib().pcclb_ring_set_small_max(self._handle, (1 << 64) - 1 if nbytes is None else int(nbytes)),
+                  "ring_set_small_max")
+
     # -- caller-buffer registration (collective, SPMD order) --
     def register(self, tensor: torch.Tensor) -> int:
         """Register a CUDA tensor on every rank (all ranks call with their

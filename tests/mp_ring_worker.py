@@ -158,7 +158,9 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             ring.restore(buf)
             check("veto restore", buf.cpu().numpy().tobytes() == mine.tobytes())
         if "registered" in scenarios:
-            # zero-copy path: peers read the registered buffer in place
+            # zero-copy path: peers read the registered buffer in place (the
+            # one-kernel small path always copies in, so it is off here)
+            ring.set_small_max_bytes(0)
             n = (1 << 22) + 5
             inputs = [np.random.default_rng(300 + p).normal(0, 2, n).astype(np.float32) for p in range(world)]
             reg = torch.empty(n + 64, dtype=torch.float32, device=dev)
@@ -202,6 +204,7 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
                 rejected = True
             check("registration mismatch rejected", rejected)
             check("registration mismatch intact", target.cpu().numpy().tobytes() == inputs[ring.position].tobytes())
+            ring.set_small_max_bytes(None)
             ring.deregister(0)
         if "qedge" in scenarios:
             # quantized schedule variants: fused at 3 and 4 CTAs/SM (slots 2, 1) and the
