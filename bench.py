@@ -462,9 +462,12 @@ def bench_allreduce(args, rank, world, local, quantize=False):
                 "algorithmic_bytes_per_gpu": hbm_bytes,
                 "nvlink_bytes_per_gpu": 2 * (world - 1) * n_c}
         # the schedule's own HBM traffic, incl. the backup the reference keeps
-        # (collective.py:501-504) and the codes peers push into this GPU:
-        # range+backup 8, per step 18, adoption 8, gather (W-1) x 6 B per n_c
-        full = (16 + 24 * (world - 1)) * n_c
+        # (collective.py:501-504) and the codes peers push into this GPU, per
+        # n_c: range+backup 8; per step 14 (quantize 4, codes in 1, backup +
+        # range 4+1+4) plus 1 from step 2 on (the previous step's codes: the
+        # running partial is recomputed, never stored); adoption 9 (x, codes,
+        # write-back); gather (W-1) x 6 (codes in + read, floats out)
+        full = (8 + 14 * (world - 1) + (world - 2) + 9 + 6 * (world - 1)) * n_c
         roof["schedule_bytes_per_gpu"] = full
         roof["frac_of_schedule_floor"] = round(full / (ms_max * 1e-3) / 1e9 / pk["hbm_gbs"], 4)
     result = {

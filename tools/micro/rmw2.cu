@@ -42,16 +42,28 @@ __device__ __forceinline__ uint4 adopt16(F4 (&in)[4], const QParams &qp) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int U>
+// V bit 1: claim also reads a volatile status word; bit 2: every other
+// position is an empty one (like the gather's B' slots)
+template <int U, int V = 0>
 __global__ void __launch_bounds__(256) direct(float *x, uint8_t *codes, uint64_t n, uint64_t item, uint32_t *claim,
                                               QParams qp) {
-  __shared__ uint32_t s_it;
+  __shared__ uint32_t s_it, s_ok;
   const uint64_t nitems = (n + item - 1) / item;
   for (;;) {
-    if (threadIdx.x == 0) s_it = atomicAdd(claim, 1u);
+    if (threadIdx.x == 0) {
+      s_it = atomicAdd(claim, 1u);
+      if (V & 1) s_ok = *(volatile uint32_t *)(claim + 1) == 0;
+    }
     __syncthreads();
-    const uint64_t it = s_it;
+    uint64_t it = s_it;
     __syncthreads();
+    if (V & 2) {
+      if (it & 1) {
+        if (it / 2 >= nitems) break;
+        continue;
+      }
+      it /= 2;
+    }
     if (it >= nitems) break;
     const uint64_t b = it * item, nv = (min(n, b + item) - b) / 16;
     for (uint64_t v = threadIdx.x; v < nv; v += 256 * U) {
@@ -283,7 +295,8 @@ int main(int argc, char **argv) {
   uint32_t *claim;
   cudaMalloc(&x, n * 4);
   cudaMalloc(&c, n);
-  cudaMalloc(&claim, 4);
+  cudaMalloc(&claim, 8);
+  cudaMemset(claim, 0, 8);
   fill<<<1184, 256>>>(x, n);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -292,6 +305,18 @@ int main(int argc, char **argv) {
   qp.scale = 2.0f / 255.0f;
   qp.inv = 1.0f / qp.scale;
   const double bytes = 9.0 * n;
+  for (int rep = 0; rep < 2; ++rep) {
+    const int g = sms * 3;
+    float a = timeit([&] { direct<2, 0><<<g, 256>>>(x, c, n, 262144, claim, qp); }, claim);
+    float b = timeit([&] { direct<2, 1><<<g, 256>>>(x, c, n, 262144, claim, qp); }, claim);
+    float d = timeit([&] { direct<2, 2><<<g, 256>>>(x, c, n, 262144, claim, qp); }, claim);
+    float e = timeit([&] { direct<2, 3><<<g, 256>>>(x, c, n, 262144, claim, qp); }, claim);
+    printf("claim variants 3 CTAs/SM 256Ki U=2: plain %.3f  +status %.3f  +skips %.3f  +both %.3f ms\n", a, b, d, e);
+  }
+  if (getenv("ONLY")) {
+    timeit([&] { direct<2><<<sms * 3, 256>>>(x, c, n, 262144, claim, qp); }, claim);
+    return 0;
+  }
   for (int per : {2, 3, 4})
     for (uint64_t item : {65536ull, 262144ull}) {
       const int g = sms * per;
