@@ -284,9 +284,23 @@ __device__ __forceinline__ uint32_t smid() {
       g_trace[i][3] = gtimer();                                     \
     }                                                               \
   }
+// per batch item: {3, nbytes of the entry << 16 | smid, start, end}
+#define TRACE_ITEM_BEGIN() const uint64_t tri_t0 = gtimer()
+#define TRACE_ITEM_END(nb)                                          \
+  if (threadIdx.x == 0) {                                           \
+    const uint32_t i = atomicAdd(&g_trace_n, 1u);                   \
+    if (i < 8192) {                                                 \
+      g_trace[i][0] = 3;                                            \
+      g_trace[i][1] = ((uint64_t)(nb) << 16) | smid();              \
+      g_trace[i][2] = tri_t0;                                       \
+      g_trace[i][3] = gtimer();                                     \
+    }                                                               \
+  }
 #else
 #define TRACE_BEGIN()
 #define TRACE_END(kind)
+#define TRACE_ITEM_BEGIN()
+#define TRACE_ITEM_END(nb)
 #endif
 
 // One launch for a batch of ordinary entries. Scratch: lanes[count x 256]
@@ -314,7 +328,9 @@ __global__ void __launch_bounds__(C::THREADS, kHashMinBlocks)
     const uint32_t e = it / G, grp = it % G;
     const HashEntry E = b.e[e];
     const uint32_t lane0 = grp * C::LANES;
+    TRACE_ITEM_BEGIN();
     const uint64_t h = hash_group<C>(E.ptr, E.nbytes, E.map, lane0, kFnvOffset, stage, bars, g);
+    TRACE_ITEM_END(E.nbytes);
     if (threadIdx.x < C::LANES) lanes[(uint64_t)e * 256 + lane0 + threadIdx.x] = h;
     if (last_part(&arrived[e], G, &s_flag)) {
       for (int j = threadIdx.x; j < 256; j += blockDim.x) lane_s[j] = __ldcg(&lanes[(uint64_t)e * 256 + j]);

@@ -15,7 +15,9 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
 dist.init_process_group("gloo")
 nb = 512 << 20
-src = torch.full((nb,), rank + 1, dtype=torch.uint8, device="cuda")
+big = os.environ.get("BIG") == "1"  # 1 GiB tensors, each rank copies the half it "owns" (rank+1)%2
+src_full = torch.full((2 * nb if big else nb,), rank + 1, dtype=torch.uint8, device="cuda")
+src = src_full
 dst = torch.empty(nb, dtype=torch.uint8, device="cuda")
 h = ctypes.create_string_buffer(64)
 off = ctypes.c_uint64()
@@ -26,25 +28,45 @@ peer = (rank + 1) % world
 p = ctypes.c_void_p()
 check(lib().pcclb_ipc_open(ctypes.create_string_buffer(allh[peer][0], 64), ctypes.byref(p)), "open")
 peer_ptr = p.value + allh[peer][1]
+own_off = ((rank + 1) % 2) * nb if big else 0
+peer_ptr += own_off
 s = torch.cuda.current_stream()
 res = {}
-for mode in ("ce", "sm"):
+for mode in ("ce", "push", "ce1g", "push_after_write", "push_after_pull"):
     times = []
     for rep in range(6):
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        if mode == "ce":
+        if mode == "ce":  # pull: local <- peer
             check(lib().pcclb_copy(dst.data_ptr(), peer_ptr, nb, s.cuda_stream), "copy")
-        else:
-            # SM copy through torch: a view over the peer pointer is not available, so use
-            # cudaMemcpy with a device-to-device kind forced through the runtime's kernel path
+        elif mode == "push":  # push: peer <- local (into the peer's src tensor: it is refilled below)
+            check(lib().pcclb_copy(peer_ptr, src_full.data_ptr() + own_off, nb, s.cuda_stream), "copy")
+        elif mode == "push_after_write":  # the source was just written by SMs (like the fold's result)
+            e0 = torch.cuda.Event(enable_timing=True)
+            dst.fill_(7)
+            e0.record(s)
+            check(lib().pcclb_copy(peer_ptr, dst.data_ptr(), nb, s.cuda_stream), "copy")
+        elif mode == "push_after_pull":  # SM remote loads of the peer buffer first (like the fold)
+            e0 = torch.cuda.Event(enable_timing=True)
+            acc = dst.view(torch.float32)
+            check(lib().pcclb_accumulate(acc.data_ptr(), peer_ptr, acc.numel(), 1, 1, s.cuda_stream), "acc")
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record(s)
+            check(lib().pcclb_copy(peer_ptr, src_full.data_ptr() + own_off, nb, s.cuda_stream), "copy")
+        else:  # two 512 MiB pulls back to back
+            check(lib().pcclb_copy(dst.data_ptr(), peer_ptr, nb, s.cuda_stream), "copy")
             check(lib().pcclb_copy(dst.data_ptr(), peer_ptr, nb, s.cuda_stream), "copy")
         e1.record(s)
         torch.cuda.synchronize()
         if rep:
             times.append(e0.elapsed_time(e1))
-    res[mode] = round(nb / (min(times) * 1e-3) / 1e9, 1)
+    res[mode] = round(nb * (2 if mode == "ce1g" else 1) / (min(times) * 1e-3) / 1e9, 1)
+    dist.barrier()
+    src.fill_(rank + 1)
+    torch.cuda.synchronize()
+    dist.barrier()
 ok = bool((dst == ((peer + 1) % 256)).all().item())
 out = [None] * world
 dist.all_gather_object(out, (res, ok))

@@ -55,3 +55,17 @@ for sm in set(g[:, 1]):
             if min(x[3], y[3]) > max(x[2], y[2]):
                 shared += 1
 print("big CTAs overlapping a batch CTA on the same SM:", shared)
+it = a[a[:, 0] == 3]
+if len(it):
+    nb = it[:, 1] >> 16
+    st, en = (it[:, 2] - t0) / 1e3, (it[:, 3] - t0) / 1e3
+    print(f"items: {len(it)}")
+    for size in sorted(set(nb.tolist()), reverse=True):
+        m = nb == size
+        d = en[m] - st[m]
+        rate = size / 2 / (d * 1e-6) / 1e9  # one lane group = half the entry
+        print(f"  entry {size / 1e6:8.1f} MB x{m.sum():4d}: start {st[m].min():6.0f}-{st[m].max():6.0f} us, "
+              f"dur {d.min():6.0f}-{np.median(d):6.0f}-{d.max():6.0f} us, per-item {np.median(rate):5.1f} GB/s, "
+              f"end max {en[m].max():6.0f}")
+    late = np.argsort(-en)[:12]
+    print("  last items (MB, start, end, sm):", [(round(nb[i] / 1e6, 1), round(st[i]), round(en[i]), int(it[i, 1] & 0xffff)) for i in late])
