@@ -17,8 +17,12 @@ dist.init_process_group("gloo")
 nb = 512 << 20
 big = os.environ.get("BIG") == "1"  # 1 GiB tensors, each rank copies the half it "owns" (rank+1)%2
 src_full = torch.full((2 * nb if big else nb,), rank + 1, dtype=torch.uint8, device="cuda")
+if os.environ.get("RAND") == "1":  # incompressible contents
+    src_full.random_(0, 256)
 src = src_full
 dst = torch.empty(nb, dtype=torch.uint8, device="cuda")
+if os.environ.get("RAND") == "1":
+    dst.random_(0, 256)
 h = ctypes.create_string_buffer(64)
 off = ctypes.c_uint64()
 check(lib().pcclb_ipc_handle(src.data_ptr(), h, ctypes.byref(off)), "h")
@@ -32,7 +36,7 @@ own_off = ((rank + 1) % 2) * nb if big else 0
 peer_ptr += own_off
 s = torch.cuda.current_stream()
 res = {}
-for mode in ("ce", "push", "ce1g", "push_after_write", "push_after_pull"):
+for mode in ("ce", "push", "ce1g", "push_after_write", "push_after_pull", "pull_then_push", "pull_sleep_push"):
     times = []
     for rep in range(6):
         dist.barrier()
@@ -55,6 +59,14 @@ for mode in ("ce", "push", "ce1g", "push_after_write", "push_after_pull"):
             dist.barrier()
             e0.record(s)
             check(lib().pcclb_copy(peer_ptr, src_full.data_ptr() + own_off, nb, s.cuda_stream), "copy")
+        elif mode in ("pull_then_push", "pull_sleep_push"):  # stream-ordered, no host sync in between
+            e0 = torch.cuda.Event(enable_timing=True)
+            acc = dst.view(torch.float32)
+            check(lib().pcclb_accumulate(acc.data_ptr(), peer_ptr, acc.numel(), 1, 1, s.cuda_stream), "acc")
+            if mode == "pull_sleep_push":
+                torch.cuda._sleep(1_000_000)  # ~0.5 ms at 1.9 GHz
+            e0.record(s)
+            check(lib().pcclb_copy(peer_ptr, src_full.data_ptr() + own_off, nb, s.cuda_stream), "copy")
         else:  # two 512 MiB pulls back to back
             check(lib().pcclb_copy(dst.data_ptr(), peer_ptr, nb, s.cuda_stream), "copy")
             check(lib().pcclb_copy(dst.data_ptr(), peer_ptr, nb, s.cuda_stream), "copy")
@@ -64,7 +76,10 @@ for mode in ("ce", "push", "ce1g", "push_after_write", "push_after_pull"):
             times.append(e0.elapsed_time(e1))
     res[mode] = round(nb * (2 if mode == "ce1g" else 1) / (min(times) * 1e-3) / 1e9, 1)
     dist.barrier()
-    src.fill_(rank + 1)
+    if os.environ.get("RAND") == "1":
+        src.random_(0, 256)
+    else:
+        src.fill_(rank + 1)
     torch.cuda.synchronize()
     dist.barrier()
 ok = bool((dst == ((peer + 1) % 256)).all().item())
