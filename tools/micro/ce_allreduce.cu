@@ -63,6 +63,10 @@ __global__ void push(const float4 *src, float4 *dst, uint64_t nv) {
 int main(int argc, char **argv) {
   const uint64_t n = argc > 1 ? strtoull(argv[1], 0, 10) : (1ull << 28);  // floats per GPU (1 GiB)
   const uint64_t half = n / 2;
+  if (n % 8 != 0) {
+    printf("n must be a multiple of 8\n");
+    return 1;
+  }
   float *buf[2], *tmp[2];
   cudaStream_t sa[2], sb[2], sc[2];
   int sms = 0;
@@ -201,6 +205,9 @@ int main(int argc, char **argv) {
   timed("sm pull+bak + ce push", [&] { run_sm_ce_bak(1, true); });
   timed("sm pull+bak + sm push", [&] { run_sm_ce_bak(1, false); });
   for (int B : {1, 2, 4, 8}) {
+    // blocks must keep 16-byte (float4) alignment: a misaligned block faults
+    // the fold kernel on both GPUs (an earlier B=3 run did exactly that)
+    if ((half / B) % 4 != 0 || half % B != 0) continue;
     char nm[64];
     snprintf(nm, sizeof nm, "ce pipeline B=%d", B);
     timed(nm, [&] { run_ce(B); });
