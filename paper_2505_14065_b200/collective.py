@@ -108,42 +108,51 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def _check_buffer(t: torch.Tensor, what: str, dtypes=(torch.float32, torch.float64, torch.bfloat16)) -> None:
+def _check_buffer(t: torch.Tensor, what: str, dtypes=(torch.float32, torch.float64, torch.bfloat16),
+                  min_numel: int = 0, device: torch.device | None = None) -> None:
+    """Every pointer handed to a kernel is checked first: a host, undersized or
+    other-device tensor is a UsageError here, never a device fault."""
     if not isinstance(t, torch.Tensor):
         raise UsageError(f"{what} must be a torch.Tensor")
     if not t.is_cuda:
         raise UsageError(f"{what} must be a CUDA tensor")
     if not t.is_contiguous():
         raise UsageError(f"{what} must be contiguous")
-    if t.dtype not in dtypes:
+    if dtypes is not None and t.dtype not in dtypes:
         raise UsageError(f"{what} has unsupported dtype {t.dtype}")
+    if t.numel() < min_numel:
+        raise UsageError(f"{what} has {t.numel()} elements, needs {min_numel}")
+    if device is not None and t.device != device:
+        raise UsageError(f"{what} is on {t.device}, the operation runs on {device}")
 
 
 def accumulate(op, acc: torch.Tensor, incoming: torch.Tensor) -> None:
     """``acc <- acc (+) incoming`` in place (np.add / np.maximum / np.minimum)."""
     op = ReduceOp.parse(op)
     _check_buffer(acc, "acc")
-    _check_buffer(incoming, "incoming")
+    _check_buffer(incoming, "incoming", device=acc.device)
     if acc.dtype != incoming.dtype or acc.numel() != incoming.numel():
         raise UsageError("acc and incoming must match in dtype and size")
-    check(
-        lib().pcclb_accumulate(
-            acc.data_ptr(), incoming.data_ptr(), acc.numel(), DTYPE_CODE[acc.dtype], op.code, _stream()
-        ),
-        "accumulate",
-    )
+    with torch.cuda.device(acc.device):
+        check(
+            lib().pcclb_accumulate(
+                acc.data_ptr(), incoming.data_ptr(), acc.numel(), DTYPE_CODE[acc.dtype], op.code, _stream()
+            ),
+            "accumulate",
+        )
 
 
 def finalize_reduction(buffer: torch.Tensor, op, world_size: int) -> None:
     """Average divides by world size; other operators are complete as-is."""
     op = ReduceOp.parse(op)
     _check_buffer(buffer, "buffer")
-    check(
-        lib().pcclb_finalize(
-            buffer.data_ptr(), buffer.numel(), DTYPE_CODE[buffer.dtype], op.code, world_size, _stream()
-        ),
-        "finalize_reduction",
-    )
+    with torch.cuda.device(buffer.device):
+        check(
+            lib().pcclb_finalize(
+                buffer.data_ptr(), buffer.numel(), DTYPE_CODE[buffer.dtype], op.code, world_size, _stream()
+            ),
+            "finalize_reduction",
+        )
 
 
 class QuantScratch:
@@ -158,24 +167,32 @@ def quantize_chunk_async(values: torch.Tensor, out: torch.Tensor, scratch: Quant
                          adopt: torch.Tensor | None = None, avg_div: int = 1) -> None:
     """Device-only quantize: range, then codes; (min, scale) land in
     ``scratch.meta`` and the non-finite flag in ``scratch.range[2]``."""
+    _check_buffer(values, "values", (torch.float32,))
     n = values.numel()
-    s = _stream()
-    L = lib()
-    check(L.pcclb_range_reset(scratch.range.data_ptr(), 1, s), "range_reset")
-    check(L.pcclb_range_f32(values.data_ptr(), n, scratch.range.data_ptr(), s), "range_f32")
-    check(
-        L.pcclb_quantize_u8(
-            values.data_ptr(),
-            n,
-            scratch.range.data_ptr(),
-            out.data_ptr(),
-            scratch.meta.data_ptr(),
-            adopt.data_ptr() if adopt is not None else None,
-            avg_div,
-            s,
-        ),
-        "quantize_u8",
-    )
+    dev = values.device
+    _check_buffer(out, "out", (torch.uint8,), n, dev)
+    _check_buffer(scratch.range, "scratch.range", (torch.int32,), 4, dev)
+    _check_buffer(scratch.meta, "scratch.meta", (torch.float32,), 2, dev)
+    if adopt is not None:
+        _check_buffer(adopt, "adopt", (torch.float32,), n, dev)
+    with torch.cuda.device(dev):
+        s = _stream()
+        L = lib()
+        check(L.pcclb_range_reset(scratch.range.data_ptr(), 1, s), "range_reset")
+        check(L.pcclb_range_f32(values.data_ptr(), n, scratch.range.data_ptr(), s), "range_f32")
+        check(
+            L.pcclb_quantize_u8(
+                values.data_ptr(),
+                n,
+                scratch.range.data_ptr(),
+                out.data_ptr(),
+                scratch.meta.data_ptr(),
+                adopt.data_ptr() if adopt is not None else None,
+                avg_div,
+                s,
+            ),
+            "quantize_u8",
+        )
 
 
 def quantize_chunk(values: torch.Tensor, out: torch.Tensor) -> tuple[float, float]:
@@ -186,10 +203,7 @@ def quantize_chunk(values: torch.Tensor, out: torch.Tensor) -> tuple[float, floa
     ValueError on non-finite input, like the reference (collective.py:117-118).
     """
     _check_buffer(values, "values", (torch.float32,))
-    if not isinstance(out, torch.Tensor) or out.dtype != torch.uint8 or not out.is_cuda:
-        raise UsageError("out must be a CUDA uint8 tensor")
-    if out.numel() < values.numel():
-        raise UsageError("out is smaller than values")
+    _check_buffer(out, "out", (torch.uint8,), values.numel(), values.device)
     if values.numel() == 0:
         return 0.0, 1.0
     scratch = QuantScratch(values.device)
@@ -209,31 +223,38 @@ def dequantize_into(codes: torch.Tensor, min_val: float, scale: float, out: torc
     """Inverse mapping x = min + q * scale, written into out (float32)."""
     _check_buffer(out, "out", (torch.float32,))
     n = out.numel()
-    if codes.numel() < n:
-        raise UsageError("codes shorter than out")
+    _check_buffer(codes, "codes", (torch.uint8,), n, out.device)
     meta = _meta_tensor(min_val, scale, out.device)
-    check(
-        lib().pcclb_dequantize_u8(out.data_ptr(), codes.data_ptr(), n, meta.data_ptr(), 1, _stream()),
-        "dequantize_u8",
-    )
+    with torch.cuda.device(out.device):
+        check(
+            lib().pcclb_dequantize_u8(out.data_ptr(), codes.data_ptr(), n, meta.data_ptr(), 1, _stream()),
+            "dequantize_u8",
+        )
 
 
 def dequant_accumulate(op, acc: torch.Tensor, codes: torch.Tensor, meta: torch.Tensor,
                        next_range: torch.Tensor | None = None) -> None:
     """Quantized reduce consume (collective.py:399-409): acc <- acc (+) D(codes)."""
     op = ReduceOp.parse(op)
-    check(
-        lib().pcclb_dequant_accumulate_u8(
-            acc.data_ptr(),
-            codes.data_ptr(),
-            acc.numel(),
-            meta.data_ptr(),
-            op.code,
-            next_range.data_ptr() if next_range is not None else None,
-            _stream(),
-        ),
-        "dequant_accumulate_u8",
-    )
+    _check_buffer(acc, "acc", (torch.float32,))
+    n, dev = acc.numel(), acc.device
+    _check_buffer(codes, "codes", (torch.uint8,), n, dev)
+    _check_buffer(meta, "meta", (torch.float32,), 2, dev)
+    if next_range is not None:
+        _check_buffer(next_range, "next_range", (torch.int32,), 4, dev)
+    with torch.cuda.device(dev):
+        check(
+            lib().pcclb_dequant_accumulate_u8(
+                acc.data_ptr(),
+                codes.data_ptr(),
+                n,
+                meta.data_ptr(),
+                op.code,
+                next_range.data_ptr() if next_range is not None else None,
+                _stream(),
+            ),
+            "dequant_accumulate_u8",
+        )
 
 
 __all__ = [

@@ -14,9 +14,13 @@ from ._native import check, lib
 from .collective import UsageError
 
 
-def _f32(t: torch.Tensor, what: str) -> None:
+def _f32(t: torch.Tensor, what: str, like: torch.Tensor | None = None) -> None:
+    """Checked before any launch (a host, short or other-device tensor is a
+    UsageError, never a device fault); `like`: same size and device."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
         raise UsageError(f"{what} must be a contiguous float32 CUDA tensor")
+    if like is not None and (t.numel() != like.numel() or t.device != like.device):
+        raise UsageError(f"{what} must match {tuple(like.shape)} on {like.device}")
 
 
 def _stream() -> int:
@@ -26,11 +30,12 @@ def _stream() -> int:
 def pseudo_gradient(global_params: torch.Tensor, local_params: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """delta = global - local (np.subtract, algos.py:334)."""
     _f32(global_params, "global_params")
-    _f32(local_params, "local_params")
+    _f32(local_params, "local_params", global_params)
     out = torch.empty_like(global_params) if out is None else out
-    _f32(out, "out")
-    check(lib().pcclb_pseudo_gradient_f32(out.data_ptr(), global_params.data_ptr(), local_params.data_ptr(),
-                                          out.numel(), _stream()), "pseudo_gradient")
+    _f32(out, "out", global_params)
+    with torch.cuda.device(out.device):
+        check(lib().pcclb_pseudo_gradient_f32(out.data_ptr(), global_params.data_ptr(), local_params.data_ptr(),
+                                              out.numel(), _stream()), "pseudo_gradient")
     return out
 
 
@@ -42,9 +47,10 @@ class PlainSGD:
 
     def step(self, params: torch.Tensor, grad: torch.Tensor) -> None:
         _f32(params, "params")
-        _f32(grad, "grad")
-        check(lib().pcclb_outer_sgd_f32(params.data_ptr(), grad.data_ptr(), params.numel(), self.lr, _stream()),
-              "outer_sgd")
+        _f32(grad, "grad", params)
+        with torch.cuda.device(params.device):
+            check(lib().pcclb_outer_sgd_f32(params.data_ptr(), grad.data_ptr(), params.numel(), self.lr, _stream()),
+                  "outer_sgd")
 
 
 class NesterovOuter:
@@ -56,10 +62,11 @@ class NesterovOuter:
         self.velocity = torch.zeros(dim, dtype=torch.float32, device=device or "cuda")
 
     def step(self, params: torch.Tensor, delta: torch.Tensor) -> None:
-        _f32(params, "params")
-        _f32(delta, "delta")
-        check(lib().pcclb_outer_nesterov_f32(params.data_ptr(), delta.data_ptr(), self.velocity.data_ptr(),
-                                             params.numel(), self.lr, self.momentum, _stream()), "outer_nesterov")
+        _f32(params, "params", self.velocity)
+        _f32(delta, "delta", self.velocity)
+        with torch.cuda.device(params.device):
+            check(lib().pcclb_outer_nesterov_f32(params.data_ptr(), delta.data_ptr(), self.velocity.data_ptr(),
+                                                 params.numel(), self.lr, self.momentum, _stream()), "outer_nesterov")
 
     def state_entries(self, prefix: str = ""):
         from .sharedstate import DType, SharedStateEntry

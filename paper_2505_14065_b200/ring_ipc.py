@@ -281,6 +281,7 @@ class DeviceRing:
 
     def restore(self, buffer: torch.Tensor) -> None:
         """Hand back the last op's input bytes (completion veto, client.py:973-983)."""
+        self._validate(buffer, ReduceOp.SUM, False)
         check(
             lib().pcclb_ring_restore(self._handle, buffer.data_ptr(), buffer.numel(), DTYPE_CODE[buffer.dtype],
                                      torch.cuda.current_stream(self.device).cuda_stream),

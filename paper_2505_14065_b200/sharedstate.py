@@ -22,6 +22,7 @@ from enum import IntEnum
 import torch
 
 from ._native import check, lib
+from .collective import UsageError
 
 FNV_OFFSET = 0xCBF29CE484222325
 FNV_PRIME = 0x100000001B3
@@ -47,10 +48,23 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def _device_bytes(t: torch.Tensor) -> tuple[int, int]:
+def _device_bytes(t: torch.Tensor, device: torch.device) -> tuple[int, int]:
+    # checked before any launch: a host or other-device pointer must be a
+    # UsageError, not a device fault
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise UsageError("hashed buffers must be CUDA tensors")
+    if t.device != device:
+        raise UsageError(f"hashed buffers must all live on {device} (got {t.device})")
     if not t.is_contiguous():
         raise ValueError("buffer must be contiguous")
     return t.data_ptr(), t.numel() * t.element_size()
+
+
+def _check_out(out: torch.Tensor, dtype: torch.dtype, n: int) -> None:
+    if not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != dtype or not out.is_contiguous():
+        raise UsageError(f"out must be a contiguous CUDA {dtype} tensor")
+    if out.numel() < n:
+        raise UsageError(f"out has {out.numel()} slots for {n} digests")
 
 
 def _to_u64(v: torch.Tensor) -> list[int]:
@@ -62,18 +76,22 @@ def simplehash_many_async(tensors: list[torch.Tensor], out: torch.Tensor) -> Non
     n = len(tensors)
     if n == 0:
         return
+    _check_out(out, torch.int64, n)
     ptrs = (ctypes.c_void_p * n)()
     sizes = (ctypes.c_uint64 * n)()
     for i, t in enumerate(tensors):
-        p, nb = _device_bytes(t)
+        p, nb = _device_bytes(t, out.device)
         ptrs[i] = p
         sizes[i] = nb
-    check(lib().pcclb_simplehash_multi(ptrs, sizes, n, out.data_ptr(), _stream()), "simplehash_multi")
+    with torch.cuda.device(out.device):
+        check(lib().pcclb_simplehash_multi(ptrs, sizes, n, out.data_ptr(), _stream()), "simplehash_multi")
 
 
 def simplehash_many(tensors: list[torch.Tensor]) -> list[int]:
     if not tensors:
         return []
+    if not isinstance(tensors[0], torch.Tensor) or not tensors[0].is_cuda:
+        raise UsageError("hashed buffers must be CUDA tensors")
     dev = tensors[0].device
     out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
     simplehash_many_async(tensors, out)
@@ -86,14 +104,18 @@ def crc32_many(tensors: list[torch.Tensor]) -> list[int]:
     n = len(tensors)
     if n == 0:
         return []
+    if not isinstance(tensors[0], torch.Tensor) or not tensors[0].is_cuda:
+        raise UsageError("crc32 buffers must be CUDA tensors")
+    dev = tensors[0].device
     ptrs = (ctypes.c_void_p * n)()
     sizes = (ctypes.c_uint64 * n)()
     for i, t in enumerate(tensors):
-        p, nb = _device_bytes(t)
+        p, nb = _device_bytes(t, dev)
         ptrs[i] = p
         sizes[i] = nb
-    out = torch.empty(n, dtype=torch.int32, device=tensors[0].device)
-    check(lib().pcclb_crc32_multi(ptrs, sizes, n, out.data_ptr(), _stream()), "crc32_multi")
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().pcclb_crc32_multi(ptrs, sizes, n, out.data_ptr(), _stream()), "crc32_multi")
     return [int(x) & 0xFFFFFFFF for x in out.cpu().tolist()]
 
 
