@@ -30,7 +30,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -194,7 +193,6 @@ def max_over_ranks(x: float, world: int) -> float:
 def bench_hash(args, rank, world, local):
     import torch
 
-    from paper_2505_14065_b200 import _native
     from paper_2505_14065_b200.sharedstate import simplehash_many_async
 
     dev = torch.device("cuda", local)

@@ -155,10 +155,9 @@ def run(rank: int, world: int, port: int, outdir: str, scenarios: list[str]) -> 
             for _, n_ in layout:
                 views.append(state[off: off + n_])
                 off += n_
-            clean = [osh_u for osh_u in []]  # filled below from the device digests
             from paper_2505_14065_b200 import simplehash_many
 
-            clean = simplehash_many(views)
+            clean = simplehash_many(views)  # digests before the drift
             drifted = 1 % world
             if rank == drifted:
                 views[0].view(torch.int16)[12345] ^= 1
