@@ -327,6 +327,41 @@ def hash_sample(layout):
     return [rng.integers(0, 256, 2 * n, dtype=np.uint8) for n in sel]
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference, pip-installed by build()
+
+
+def reference_own_hash(bufs, want=None, max_bytes=1200 << 20) -> dict | None:
+    """The reference's own ``churncomm.sharedstate.simplehash`` (SURVEY 8(d)
+    (iv)), timed beside the C port on part of the same sample: workers=1, its
+    fastest setting (2 / 4 / 8 workers measured 0.28 / 0.14 / 0.07 GB/s against
+    0.50). Reported only; the port stays the baseline value. ``want``: the
+    port's digests of ``bufs``, compared with the reference's own."""
+    if not os.path.isdir(os.path.join(REF_PKG, "churncomm")):
+        return None
+    sys.path.insert(0, REF_PKG)
+    try:
+        from churncomm import sharedstate as ref_ss
+    except Exception as e:  # noqa: BLE001 - report, never fail the bench line
+        return {"unavailable": f"{type(e).__name__}: {e}"[:160]}
+    finally:
+        sys.path.remove(REF_PKG)
+    picked, nb = [], 0
+    for i in sorted(range(len(bufs)), key=lambda i: bufs[i].size):
+        if nb + bufs[i].size > max_bytes and picked:
+            break
+        picked.append(i)
+        nb += bufs[i].size
+    t = time.perf_counter()
+    got = [ref_ss.simplehash(bufs[i], workers=1) for i in picked]
+    dt = time.perf_counter() - t
+    d = {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
+         "impl": "churncomm.sharedstate.simplehash(buffer, workers=1), unmodified reference (baseline/_ref)",
+         "sample": f"{len(picked)} of the sample's entries ({nb / 1e6:.0f} MB)"}
+    if want is not None:
+        d["digests_equal_port"] = all(int(got[k]) == int(want[i]) for k, i in enumerate(picked))
+    return d
+
+
 def cpu_hash_baseline(layout) -> dict:
     from oracle import simplehash as osh
 
@@ -334,10 +369,14 @@ def cpu_hash_baseline(layout) -> dict:
     threads = os.cpu_count() or 1
     nb = sum(b.size for b in bufs)
     t = time.perf_counter()
-    osh.simplehash_many_c(bufs, threads=threads)
+    want = osh.simplehash_many_c(bufs, threads=threads)
     dt = time.perf_counter() - t
-    return {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"{len(bufs)} of 291 config-4 entries ({nb / 1e9:.2f} GB), oracle/simplehash.c on {threads} threads"}
+    out = {"value": round(nb / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"{len(bufs)} of 291 config-4 entries ({nb / 1e9:.2f} GB), oracle/simplehash.c on {threads} threads"}
+    own = reference_own_hash(bufs, want)
+    if own is not None:
+        out["reference_own"] = own
+    return out
 
 
 def bench_allreduce(args, rank, world, local, quantize=False):
@@ -670,15 +709,19 @@ def reference_arm(args, workload, world):
         t = time.perf_counter()
         steps = max(1, min(args.steps, 2))
         for _ in range(steps):
-            osh.simplehash_many_c(bufs, threads=threads)
+            want = osh.simplehash_many_c(bufs, threads=threads)
         dt = (time.perf_counter() - t) / steps
         v = round(world * nb / dt / 1e9, 3)
+        cpu = {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"{len(bufs)} of 291 entries ({nb / 1e9:.2f} GB) via oracle/simplehash.c"}
+        own = reference_own_hash(bufs, want)
+        if own is not None:
+            cpu["reference_own"] = own
         return {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": world,
                 "steps": steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {"workload": "config4-hash (bounded sample)"},
-                "cpu_baseline": {"value": v, "unit": "GB/s", "cores": threads, "kind": "port",
-                                 "sample": f"{len(bufs)} of 291 entries ({nb / 1e9:.2f} GB) via oracle/simplehash.c"},
+                "cpu_baseline": cpu,
                 "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     from oracle import ring as oring
 

@@ -13,7 +13,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("workload,world", [("allreduce", 2), ("quant", 4), ("async", 2)])
+@pytest.mark.parametrize("workload,world", [("allreduce", 2), ("quant", 4), ("async", 2), ("hash", 1)])
 def test_reference_arm_json(workload, world):
     env = dict(os.environ, WORLD_SIZE=str(world), RANK="0")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", workload,
@@ -25,6 +25,10 @@ def test_reference_arm_json(workload, world):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0 and line["n_gpus"] == world
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    own = line["cpu_baseline"].get("reference_own")
+    if workload == "hash" and own is not None and "unavailable" not in own:
+        # the reference's own simplehash, timed beside the port, agrees with it
+        assert own["digests_equal_port"] and own["value"] > 0
 
 
 def test_reference_arm_nonzero_rank_is_silent():
